@@ -1,0 +1,168 @@
+/*
+ * tricontact_b200.h -- C ABI of the B200 (sm_100a) triangle-pair contact
+ * kernels: the drop-in boundary for the reference's hot path
+ * (/root/reference/pkg/src/tricontact/kernels.py, "RK" below).
+ *
+ * Every entry point takes plain pointers and sizes; no torch types.  Two
+ * families:
+ *
+ *  - device entry points (tc_<variant>_<dtype>): all array pointers are
+ *    DEVICE pointers, work is enqueued on `stream` (a cudaStream_t passed as
+ *    void*, NULL = legacy default stream) and the call returns without
+ *    synchronising.  Return code reports argument/launch errors only;
+ *    per-pair degenerate failures are reported through tc_stats.degenerate
+ *    and kind == TC_KIND_DEGENERATE.
+ *  - host entry points (tc_<variant>_host_<dtype>): all array pointers are
+ *    HOST pointers (pinned memory makes the copies asynchronous DMA); the
+ *    library pipelines H2D copy / kernel / D2H copy over chunks on its own
+ *    streams and returns after the results are on the host.  The hybrid host
+ *    call returns TC_EDEGENERATE when a fallback pair was degenerate (the
+ *    reference raises DegenerateTriangle there, RK/kernels.py:598-600).
+ *
+ * Layout (flags & TC_SOA == 0, the reference's own, RK/geometry.py:35-42):
+ *   tri_a, tri_b: (n, 3, 3) vertex-major triangles, 9 scalars per triangle;
+ *   point_a/point_b: (n, 3); bary_a/bary_b: (n, 2); distance, kind: (n,).
+ * With TC_SOA: tri_a / tri_b are planar [9][n] (plane 3*v + c holds vertex v
+ * coordinate c of every pair); point_* are [3][n] and bary_* [2][n] planes.
+ * Any output pointer may be NULL (not written); with all of them NULL the
+ * call is reduce-only (tc_stats).
+ */
+#ifndef TRICONTACT_B200_H
+#define TRICONTACT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TC_ABI_VERSION 1
+
+/* return codes */
+#define TC_OK 0
+#define TC_EINVAL 1          /* bad argument (n < 0, NULL input, bad params) */
+#define TC_EDEGENERATE 2     /* host hybrid: some fallback pair was degenerate */
+#define TC_ECUDA 3           /* CUDA runtime error (tc_last_error() has the text) */
+#define TC_ENODEVICE 4       /* no usable sm_100 device */
+
+/* kind values, RK/kernels.py:36-39 (+ DEGENERATE, set only by hybrid) */
+#define TC_KIND_NO_CONTACT 0
+#define TC_KIND_CONTACT 1
+#define TC_KIND_NOT_TERMINATED 2
+#define TC_KIND_DEGENERATE 3
+
+/* flags (tc_params.flags) */
+#define TC_SOA 1u       /* planar inputs/outputs, see above */
+#define TC_STRICT 2u    /* numpy-order rounding: no FMA contraction, 3-term dot in the
+                           reference's einsum order; bit-identical to the reference */
+#define TC_EMIT_IDS 4u  /* write ids (4 bytes per pair, layout in DESIGN.md) */
+
+/* RK/kernels.py:42-72 KernelParams, plus flags. */
+typedef struct {
+    double epsilon;            /* halo width used when eps == NULL */
+    double c_factor;           /* functional-change settle factor */
+    double alpha_iterative;    /* penalty weight factor (x max squared edge) */
+    double alpha_regulariser;  /* diagonal regulariser factor (x max squared edge) */
+    double move_factor;        /* contact-point-movement settle factor */
+    double start_coord;        /* initial barycentric coordinate */
+    int32_t n_iterative;       /* fixed sweep count */
+    uint32_t flags;            /* TC_SOA | TC_STRICT | TC_EMIT_IDS */
+} tc_params;
+
+/* Device-resident tallies, accumulated atomically (monotone, like
+ * KernelCounters RK/kernels.py:75-93) until reset with tc_stats_reset. */
+typedef struct {
+    int64_t iterative;    /* iterative_invocations */
+    int64_t comparison;   /* comparison_invocations */
+    int64_t fallback;     /* fallback_invocations */
+    int64_t degenerate;   /* fallback pairs with a degenerate triangle */
+    int64_t contacts;     /* pairs whose final kind is CONTACT */
+    double min_distance;  /* min final distance over non-degenerate pairs (+inf if none) */
+} tc_stats;
+
+/* Fill p with the reference defaults (RK/kernels.py:56-62). */
+void tc_params_default(tc_params* p);
+int tc_abi_version(void);
+const char* tc_last_error(void);
+
+/* Zero the counters and set min_distance = +inf (device pointer). */
+int tc_stats_reset(tc_stats* stats, void* stream);
+
+/* ---- device entry points ------------------------------------------------
+ * eps: per-pair halo (n,) or NULL for p->epsilon (RK/kernels.py:143-149).
+ * allow_fb: per-pair fallback mask (n,) uint8 or NULL for "all" (RK/kernels.py:589-593).
+ * stats: device tc_stats or NULL. */
+
+/* RK/kernels.py:301 comparison_batch */
+int tc_comparison_f64(const double* tri_a, const double* tri_b, int64_t n, const double* eps,
+                      const tc_params* p, double* distance, double* point_a, double* point_b,
+                      double* bary_a, double* bary_b, int8_t* kind, uint8_t* ids,
+                      tc_stats* stats, void* stream);
+int tc_comparison_f32(const float* tri_a, const float* tri_b, int64_t n, const float* eps,
+                      const tc_params* p, float* distance, float* point_a, float* point_b,
+                      float* bary_a, float* bary_b, int8_t* kind, uint8_t* ids,
+                      tc_stats* stats, void* stream);
+
+/* RK/kernels.py:447 iterative_batch */
+int tc_iterative_f64(const double* tri_a, const double* tri_b, int64_t n, const double* eps,
+                     const tc_params* p, double* distance, double* point_a, double* point_b,
+                     double* bary_a, double* bary_b, int8_t* kind, uint8_t* ids,
+                     tc_stats* stats, void* stream);
+int tc_iterative_f32(const float* tri_a, const float* tri_b, int64_t n, const float* eps,
+                     const tc_params* p, float* distance, float* point_a, float* point_b,
+                     float* bary_a, float* bary_b, int8_t* kind, uint8_t* ids,
+                     tc_stats* stats, void* stream);
+
+/* RK/kernels.py:568 hybrid_batch: iterative, then in-kernel comparison fallback
+ * for NOT_TERMINATED pairs with allow_fb set; degenerate fallback pairs keep
+ * the iterative result with kind TC_KIND_DEGENERATE. */
+int tc_hybrid_f64(const double* tri_a, const double* tri_b, int64_t n, const double* eps,
+                  const uint8_t* allow_fb, const tc_params* p, double* distance,
+                  double* point_a, double* point_b, double* bary_a, double* bary_b,
+                  int8_t* kind, uint8_t* ids, tc_stats* stats, void* stream);
+int tc_hybrid_f32(const float* tri_a, const float* tri_b, int64_t n, const float* eps,
+                  const uint8_t* allow_fb, const tc_params* p, float* distance,
+                  float* point_a, float* point_b, float* bary_a, float* bary_b,
+                  int8_t* kind, uint8_t* ids, tc_stats* stats, void* stream);
+
+/* RK/kernels.py:157 closest_point_triangle_batch: points (n,3), tris (n,3,3). */
+int tc_closest_point_triangle_f64(const double* points, const double* tris, int64_t n,
+                                  double* closest, double* bary, void* stream);
+int tc_closest_point_triangle_f32(const float* points, const float* tris, int64_t n,
+                                  float* closest, float* bary, void* stream);
+
+/* RK/geometry.py:68 degenerate_mask (rel_tol 1e-12): tris (n,3,3) -> mask (n,). */
+int tc_degenerate_mask_f64(const double* tris, int64_t n, uint8_t* mask, void* stream);
+int tc_degenerate_mask_f32(const float* tris, int64_t n, uint8_t* mask, void* stream);
+
+/* ---- host entry points ----------------------------------------------------
+ * Same arguments with HOST pointers; variant: 0 comparison, 1 iterative,
+ * 2 hybrid.  stats (host, may be NULL) receives this call's tallies
+ * (accumulated into *stats).  Synchronous. */
+#define TC_VARIANT_COMPARISON 0
+#define TC_VARIANT_ITERATIVE 1
+#define TC_VARIANT_HYBRID 2
+int tc_run_host_f64(int variant, const double* tri_a, const double* tri_b, int64_t n,
+                    const double* eps, const uint8_t* allow_fb, const tc_params* p,
+                    double* distance, double* point_a, double* point_b, double* bary_a,
+                    double* bary_b, int8_t* kind, uint8_t* ids, tc_stats* stats);
+int tc_run_host_f32(int variant, const float* tri_a, const float* tri_b, int64_t n,
+                    const float* eps, const uint8_t* allow_fb, const tc_params* p,
+                    float* distance, float* point_a, float* point_b, float* bary_a,
+                    float* bary_b, int8_t* kind, uint8_t* ids, tc_stats* stats);
+
+/* Host-pointer versions of the two helpers above (synchronous). */
+int tc_closest_point_triangle_host_f64(const double* points, const double* tris, int64_t n,
+                                       double* closest, double* bary);
+int tc_closest_point_triangle_host_f32(const float* points, const float* tris, int64_t n,
+                                       float* closest, float* bary);
+int tc_degenerate_mask_host_f64(const double* tris, int64_t n, uint8_t* mask);
+int tc_degenerate_mask_host_f32(const float* tris, int64_t n, uint8_t* mask);
+
+/* Number of kernel launches this library has enqueued since load. */
+int64_t tc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRICONTACT_B200_H */

@@ -1,0 +1,115 @@
+"""ctypes binding of include/tricontact_b200.h (libtricontact_b200.so).
+
+This is the reference-side binding a maintainer would add: every symbol the
+header declares is bound here with its exact C signature.  There is no CPU
+fallback -- if the library is missing or no CUDA device is present, the
+product entry points raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libtricontact_b200.so"
+
+TC_OK, TC_EINVAL, TC_EDEGENERATE, TC_ECUDA, TC_ENODEVICE = 0, 1, 2, 3, 4
+TC_SOA, TC_STRICT, TC_EMIT_IDS = 1, 2, 4
+VARIANTS = {"comparison": 0, "iterative": 1, "hybrid": 2}
+
+
+class TcParams(ctypes.Structure):
+    _fields_ = [
+        ("epsilon", ctypes.c_double),
+        ("c_factor", ctypes.c_double),
+        ("alpha_iterative", ctypes.c_double),
+        ("alpha_regulariser", ctypes.c_double),
+        ("move_factor", ctypes.c_double),
+        ("start_coord", ctypes.c_double),
+        ("n_iterative", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
+    ]
+
+
+class TcStats(ctypes.Structure):
+    _fields_ = [
+        ("iterative", ctypes.c_int64),
+        ("comparison", ctypes.c_int64),
+        ("fallback", ctypes.c_int64),
+        ("degenerate", ctypes.c_int64),
+        ("contacts", ctypes.c_int64),
+        ("min_distance", ctypes.c_double),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_INT = ctypes.c_int
+
+# symbol -> (restype, argtypes); mirrors include/tricontact_b200.h one to one
+SIGNATURES = {
+    "tc_params_default": (None, [_P]),
+    "tc_abi_version": (_INT, []),
+    "tc_last_error": (ctypes.c_char_p, []),
+    "tc_launch_count": (_I64, []),
+    "tc_stats_reset": (_INT, [_P, _P]),
+    "tc_closest_point_triangle_f64": (_INT, [_P, _P, _I64, _P, _P, _P]),
+    "tc_closest_point_triangle_f32": (_INT, [_P, _P, _I64, _P, _P, _P]),
+    "tc_degenerate_mask_f64": (_INT, [_P, _I64, _P, _P]),
+    "tc_degenerate_mask_f32": (_INT, [_P, _I64, _P, _P]),
+    "tc_closest_point_triangle_host_f64": (_INT, [_P, _P, _I64, _P, _P]),
+    "tc_closest_point_triangle_host_f32": (_INT, [_P, _P, _I64, _P, _P]),
+    "tc_degenerate_mask_host_f64": (_INT, [_P, _I64, _P]),
+    "tc_degenerate_mask_host_f32": (_INT, [_P, _I64, _P]),
+    "tc_run_host_f64": (_INT, [_INT, _P, _P, _I64, _P, _P, _P] + [_P] * 7 + [_P]),
+    "tc_run_host_f32": (_INT, [_INT, _P, _P, _I64, _P, _P, _P] + [_P] * 7 + [_P]),
+}
+for _v in ("comparison", "iterative"):
+    for _s in ("f64", "f32"):
+        # tri_a, tri_b, n, eps, p, distance, point_a, point_b, bary_a, bary_b, kind, ids, stats, stream
+        SIGNATURES[f"tc_{_v}_{_s}"] = (_INT, [_P, _P, _I64, _P, _P] + [_P] * 7 + [_P, _P])
+for _s in ("f64", "f32"):
+    # tri_a, tri_b, n, eps, allow_fb, p, distance, ..., ids, stats, stream
+    SIGNATURES[f"tc_hybrid_{_s}"] = (_INT, [_P, _P, _I64, _P, _P, _P] + [_P] * 7 + [_P, _P])
+
+_lib = None
+
+
+class TricontactError(RuntimeError):
+    pass
+
+
+def load(path: Path | str | None = None):
+    """Load the library and bind every header symbol (raises if absent)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise TricontactError(
+            f"{p} is missing: build it with `python -m paper_2105_12415_b200._build` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = "tricontact call"):
+    if rc != TC_OK:
+        msg = load().tc_last_error()
+        raise TricontactError(f"{what} failed with code {rc}: {msg.decode() if msg else ''}")
+
+
+def params_struct(params, flags: int = 0) -> TcParams:
+    """KernelParams-like object -> TcParams."""
+    return TcParams(float(params.epsilon), float(params.c_factor), float(params.alpha_iterative),
+                    float(params.alpha_regulariser), float(params.move_factor), float(params.start_coord),
+                    int(params.n_iterative), int(flags))

@@ -1,0 +1,671 @@
+// tc_kernels.cu -- sm_100a kernels and the C ABI of include/tricontact_b200.h.
+//
+// Kernels (one triangle pair per thread, grid-stride / persistent over the
+// pair range, grid sized to the SM count x resident CTAs per SM):
+//   comparison_kernel  RK/kernels.py:301-401
+//   iterative_kernel   RK/kernels.py:447-565
+//   hybrid_kernel      RK/kernels.py:568-605 -- iterative for a tile of
+//       BLOCK pairs, NOT_TERMINATED lanes (with allow_fb) are appended to a
+//       shared-memory queue by warp ballot; whenever the queue holds a full
+//       block of pairs, all BLOCK threads run the comparison kernel on it, so
+//       the divergent fallback executes on full warps.  The fallback never
+//       leaves the kernel.
+//   cpt_kernel / degenerate_kernel: RK/kernels.py:157, RK/geometry.py:68.
+// Every kernel reduces its tallies per CTA (warp shuffles) and folds them
+// into a device tc_stats with one set of atomics per CTA.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "tc_pair.cuh"
+#include "../../include/tricontact_b200.h"
+
+namespace tc {
+
+constexpr int BLOCK = 256;
+
+static std::atomic<int64_t> g_launches{0};
+static thread_local char g_err[512] = "";
+
+static int set_err(const char* what, cudaError_t e) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return TC_ECUDA;
+}
+
+template <typename T>
+struct Args {
+    const T* tri_a;
+    const T* tri_b;
+    int64_t n;
+    const T* eps;
+    T eps_scalar;
+    const uint8_t* allow;
+    T* distance;
+    T* pa;
+    T* pb;
+    T* ba;
+    T* bb;
+    int8_t* kind;
+    uint8_t* ids;
+    tc_stats* stats;
+    double c_factor, alpha_it, alpha_reg, move_factor, start_coord;
+    int n_iterative;
+};
+
+template <class R, typename T>
+__device__ __forceinline__ KP<R> make_kp(const Args<T>& a) {
+    KP<R> k;
+    k.c_factor = R(T(a.c_factor));
+    k.alpha_it = R(T(a.alpha_it));
+    k.alpha_reg = R(T(a.alpha_reg));
+    k.move_factor = R(T(a.move_factor));
+    k.start_coord = R(T(a.start_coord));
+    k.n_iterative = a.n_iterative;
+    return k;
+}
+
+// ---- loads / stores ---------------------------------------------------------
+template <bool SOA, class R, typename T>
+__device__ __forceinline__ void load_tri(const T* __restrict__ src, int64_t i, int64_t n, R* t) {
+    if (SOA) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) t[k] = R(__ldg(src + k * n + i));
+    } else {
+        const T* p = src + 9 * i;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) t[k] = R(__ldg(p + k));
+    }
+}
+
+template <bool SOA, class R, typename T>
+__device__ __forceinline__ void store_rec(const Args<T>& a, int64_t i, const Rec<R>& r) {
+    const int64_t n = a.n;
+    if (a.distance) a.distance[i] = val(r.distance);
+    if (a.kind) a.kind[i] = (int8_t)r.kind;
+    if (SOA) {
+        if (a.pa) { a.pa[i] = val(r.pa[0]); a.pa[n + i] = val(r.pa[1]); a.pa[2 * n + i] = val(r.pa[2]); }
+        if (a.pb) { a.pb[i] = val(r.pb[0]); a.pb[n + i] = val(r.pb[1]); a.pb[2 * n + i] = val(r.pb[2]); }
+        if (a.ba) { a.ba[i] = val(r.ba[0]); a.ba[n + i] = val(r.ba[1]); }
+        if (a.bb) { a.bb[i] = val(r.bb[0]); a.bb[n + i] = val(r.bb[1]); }
+    } else {
+        if (a.pa) { a.pa[3 * i] = val(r.pa[0]); a.pa[3 * i + 1] = val(r.pa[1]); a.pa[3 * i + 2] = val(r.pa[2]); }
+        if (a.pb) { a.pb[3 * i] = val(r.pb[0]); a.pb[3 * i + 1] = val(r.pb[1]); a.pb[3 * i + 2] = val(r.pb[2]); }
+        if (a.ba) { a.ba[2 * i] = val(r.ba[0]); a.ba[2 * i + 1] = val(r.ba[1]); }
+        if (a.bb) { a.bb[2 * i] = val(r.bb[0]); a.bb[2 * i + 1] = val(r.bb[1]); }
+    }
+    if (a.ids) {
+        uint8_t* p = a.ids + 4 * i;
+        if ((reinterpret_cast<uintptr_t>(p) & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(p) = r.ids;
+        } else {
+            p[0] = r.ids & 0xFF; p[1] = (r.ids >> 8) & 0xFF; p[2] = (r.ids >> 16) & 0xFF; p[3] = r.ids >> 24;
+        }
+    }
+}
+
+// ---- per-CTA tallies -> tc_stats ----------------------------------------------
+struct Tally {
+    unsigned long long iterative = 0, comparison = 0, degenerate = 0, contacts = 0;
+    double min_d = __builtin_huge_val();
+
+    template <class R>
+    __device__ __forceinline__ void result(const Rec<R>& r) {
+        if (r.kind == KIND_DEGENERATE) return;
+        contacts += (r.kind == KIND_CONTACT);
+        const double d = (double)val(r.distance) + 0.0;  // -0 -> +0
+        min_d = (d < min_d) ? d : min_d;
+    }
+
+    // COMPARISON_IS_FALLBACK: hybrid comparisons also count as fallbacks
+    template <bool COMPARISON_IS_FALLBACK>
+    __device__ void flush(tc_stats* s) {
+        if (!s) return;
+        __shared__ unsigned long long red[5][BLOCK / 32];
+        __shared__ double redm[BLOCK / 32];
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            iterative += __shfl_xor_sync(0xffffffffu, iterative, off);
+            comparison += __shfl_xor_sync(0xffffffffu, comparison, off);
+            degenerate += __shfl_xor_sync(0xffffffffu, degenerate, off);
+            contacts += __shfl_xor_sync(0xffffffffu, contacts, off);
+            const double o = __shfl_xor_sync(0xffffffffu, min_d, off);
+            min_d = (o < min_d) ? o : min_d;
+        }
+        if (lane == 0) {
+            red[0][wid] = iterative; red[1][wid] = comparison; red[2][wid] = degenerate; red[3][wid] = contacts;
+            redm[wid] = min_d;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long v[4] = {0, 0, 0, 0};
+            double m = __builtin_huge_val();
+            for (int w = 0; w < BLOCK / 32; ++w) {
+                for (int k = 0; k < 4; ++k) v[k] += red[k][w];
+                m = (redm[w] < m) ? redm[w] : m;
+            }
+            auto* c = reinterpret_cast<unsigned long long*>(s);
+            if (v[0]) atomicAdd(c + 0, v[0]);
+            if (v[1]) {
+                atomicAdd(c + 1, v[1]);
+                if (COMPARISON_IS_FALLBACK) atomicAdd(c + 2, v[1]);
+            }
+            if (v[2]) atomicAdd(c + 3, v[2]);
+            if (v[3]) atomicAdd(c + 4, v[3]);
+            // distances are >= 0 (or NaN, skipped): IEEE order == unsigned bit order
+            if (m == m && m < __builtin_huge_val())
+                atomicMin(reinterpret_cast<unsigned long long*>(&s->min_distance),
+                          (unsigned long long)__double_as_longlong(m));
+        }
+    }
+};
+
+template <typename T, bool STRICT>
+struct Pol { using R = T; };
+template <typename T>
+struct Pol<T, true> { using R = Strict<T>; };
+
+// ---- kernels ---------------------------------------------------------------------
+template <typename T, bool STRICT, bool SOA>
+__global__ void __launch_bounds__(BLOCK) comparison_kernel(Args<T> a) {
+    using R = typename Pol<T, STRICT>::R;
+    Tally tl;
+    for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BLOCK) {
+        R A[9], B[9];
+        load_tri<SOA>(a.tri_a, i, a.n, A);
+        load_tri<SOA>(a.tri_b, i, a.n, B);
+        const R eps = R(a.eps ? a.eps[i] : a.eps_scalar);
+        Rec<R> r;
+        comparison_pair(A, B, eps, r);
+        store_rec<SOA>(a, i, r);
+        tl.comparison++;
+        tl.result(r);
+    }
+    // comparison_batch alone counts as comparison work but not as a fallback
+    tl.flush<false>(a.stats);
+}
+
+template <typename T, bool STRICT, bool SOA>
+__global__ void __launch_bounds__(BLOCK) iterative_kernel(Args<T> a) {
+    using R = typename Pol<T, STRICT>::R;
+    const KP<R> kp = make_kp<R>(a);
+    Tally tl;
+    for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BLOCK) {
+        R A[9], B[9];
+        load_tri<SOA>(a.tri_a, i, a.n, A);
+        load_tri<SOA>(a.tri_b, i, a.n, B);
+        const R eps = R(a.eps ? a.eps[i] : a.eps_scalar);
+        Rec<R> r;
+        iterative_pair(A, B, eps, kp, r);
+        store_rec<SOA>(a, i, r);
+        tl.iterative++;
+        tl.result(r);
+    }
+    tl.flush<false>(a.stats);
+}
+
+template <typename T, bool STRICT, bool SOA>
+__global__ void __launch_bounds__(BLOCK) hybrid_kernel(Args<T> a) {
+    using R = typename Pol<T, STRICT>::R;
+    __shared__ int64_t queue[2 * BLOCK];
+    __shared__ int qn;
+    const KP<R> kp = make_kp<R>(a);
+    Tally tl;
+    if (threadIdx.x == 0) qn = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
+
+    auto fallback = [&](int64_t j) {
+        R A[9], B[9];
+        load_tri<SOA>(a.tri_a, j, a.n, A);
+        load_tri<SOA>(a.tri_b, j, a.n, B);
+        const R eps = R(a.eps ? a.eps[j] : a.eps_scalar);
+        Rec<R> r;
+        comparison_pair(A, B, eps, r);
+        // the pair was open (not settled) in the iterative pass
+        r.ids |= (uint32_t)FLAG_FALLBACK << 24;
+        store_rec<SOA>(a, j, r);
+        tl.comparison++;
+        tl.result(r);
+    };
+
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t i = tile * BLOCK + threadIdx.x;
+        bool enq = false;
+        if (i < a.n) {
+            R A[9], B[9];
+            load_tri<SOA>(a.tri_a, i, a.n, A);
+            load_tri<SOA>(a.tri_b, i, a.n, B);
+            const R eps = R(a.eps ? a.eps[i] : a.eps_scalar);
+            Rec<R> r;
+            iterative_pair(A, B, eps, kp, r);
+            tl.iterative++;
+            if (r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i])) {
+                if (degenerate_tri(A) || degenerate_tri(B)) {
+                    r.kind = KIND_DEGENERATE;
+                    r.ids |= (uint32_t)FLAG_DEGENERATE << 24;
+                    tl.degenerate++;
+                } else {
+                    enq = true;
+                }
+            }
+            if (!enq) {
+                store_rec<SOA>(a, i, r);
+                tl.result(r);
+            }
+        }
+        // warp-aggregated append to the block queue
+        const unsigned m = __ballot_sync(0xffffffffu, enq);
+        if (m) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&qn, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (enq) queue[base + __popc(m & ((1u << lane) - 1u))] = i;
+        }
+        __syncthreads();
+        const int q = qn;
+        if (q >= BLOCK) {
+            // a full block of open pairs: every thread takes one
+            fallback(queue[q - BLOCK + threadIdx.x]);
+            __syncthreads();
+            if (threadIdx.x == 0) qn = q - BLOCK;
+        }
+        __syncthreads();
+    }
+    const int q = qn;
+    if (threadIdx.x < q) fallback(queue[threadIdx.x]);
+    tl.flush<true>(a.stats);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(BLOCK) cpt_kernel(const T* P, const T* Tr, int64_t n, T* closest, T* bary) {
+    using R = Strict<T>;
+    for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
+        R p[3], t[9], c[3], u, w;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) p[k] = R(P[3 * i + k]);
+#pragma unroll
+        for (int k = 0; k < 9; ++k) t[k] = R(Tr[9 * i + k]);
+        closest_point_triangle(p, t, c, u, w);
+        if (closest) { closest[3 * i] = c[0].v; closest[3 * i + 1] = c[1].v; closest[3 * i + 2] = c[2].v; }
+        if (bary) { bary[2 * i] = u.v; bary[2 * i + 1] = w.v; }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(BLOCK) degenerate_kernel(const T* Tr, int64_t n, uint8_t* mask) {
+    using R = Strict<T>;
+    for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
+        R t[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) t[k] = R(Tr[9 * i + k]);
+        mask[i] = degenerate_tri(t) ? 1 : 0;
+    }
+}
+
+__global__ void stats_reset_kernel(tc_stats* s) {
+    s->iterative = s->comparison = s->fallback = s->degenerate = s->contacts = 0;
+    s->min_distance = __builtin_huge_val();
+}
+
+// ---- launch helpers ------------------------------------------------------------------
+static int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <typename K>
+static int64_t grid_for(K kernel, int64_t n) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int64_t tiles = (n + BLOCK - 1) / BLOCK;
+    const int64_t full = (int64_t)sm_count() * per_sm;
+    return tiles < full ? tiles : full;
+}
+
+enum Variant { V_COMPARISON = 0, V_ITERATIVE = 1, V_HYBRID = 2 };
+
+template <typename T, bool STRICT, bool SOA>
+static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
+    if (variant == V_COMPARISON) {
+        auto k = comparison_kernel<T, STRICT, SOA>;
+        k<<<(unsigned)grid_for(k, a.n), BLOCK, 0, s>>>(a);
+    } else if (variant == V_ITERATIVE) {
+        auto k = iterative_kernel<T, STRICT, SOA>;
+        k<<<(unsigned)grid_for(k, a.n), BLOCK, 0, s>>>(a);
+    } else {
+        auto k = hybrid_kernel<T, STRICT, SOA>;
+        k<<<(unsigned)grid_for(k, a.n), BLOCK, 0, s>>>(a);
+    }
+    g_launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TC_OK : set_err("kernel launch", e);
+}
+
+static bool params_ok(const tc_params* p) {
+    return p && p->epsilon > 0.0 && p->n_iterative >= 1 && p->c_factor > 0.0 && p->alpha_iterative > 0.0 &&
+           p->alpha_regulariser > 0.0;
+}
+
+template <typename T>
+static int run_device(int variant, const T* tri_a, const T* tri_b, int64_t n, const T* eps, const uint8_t* allow,
+                      const tc_params* p, T* distance, T* pa, T* pb, T* ba, T* bb, int8_t* kind, uint8_t* ids,
+                      tc_stats* stats, void* stream) {
+    if (n < 0 || !params_ok(p)) {
+        snprintf(g_err, sizeof(g_err), "invalid argument (n=%lld or params)", (long long)n);
+        return TC_EINVAL;
+    }
+    if (n == 0) return TC_OK;
+    if (!tri_a || !tri_b) {
+        snprintf(g_err, sizeof(g_err), "NULL triangle input");
+        return TC_EINVAL;
+    }
+    Args<T> a;
+    a.tri_a = tri_a; a.tri_b = tri_b; a.n = n; a.eps = eps; a.eps_scalar = (T)p->epsilon; a.allow = allow;
+    a.distance = distance; a.pa = pa; a.pb = pb; a.ba = ba; a.bb = bb; a.kind = kind;
+    a.ids = (p->flags & TC_EMIT_IDS) ? ids : nullptr;
+    a.stats = stats;
+    a.c_factor = p->c_factor; a.alpha_it = p->alpha_iterative; a.alpha_reg = p->alpha_regulariser;
+    a.move_factor = p->move_factor; a.start_coord = p->start_coord; a.n_iterative = p->n_iterative;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const bool strict = p->flags & TC_STRICT, soa = p->flags & TC_SOA;
+    if (strict) return soa ? launch3<T, true, true>(variant, a, s) : launch3<T, true, false>(variant, a, s);
+    return soa ? launch3<T, false, true>(variant, a, s) : launch3<T, false, false>(variant, a, s);
+}
+
+// ---- host pipeline ----------------------------------------------------------------------
+// Chunks of the pair range are staged through per-stream device buffers:
+// H2D(c) on stream c % NS, then the kernel, then D2H -- so the copies of one
+// chunk overlap the kernel of its neighbours.
+struct HostCtx {
+    static constexpr int NS = 3;
+    std::mutex mu;
+    bool init = false;
+    cudaStream_t st[NS];
+    void* buf[NS] = {nullptr, nullptr, nullptr};
+    size_t cap = 0;
+    tc_stats* dstats = nullptr;
+};
+static HostCtx g_host;
+
+template <typename T>
+static int run_host(int variant, const T* tri_a, const T* tri_b, int64_t n, const T* eps, const uint8_t* allow,
+                    const tc_params* p, T* distance, T* pa, T* pb, T* ba, T* bb, int8_t* kind, uint8_t* ids,
+                    tc_stats* stats) {
+    if (n < 0 || !params_ok(p) || (n > 0 && (!tri_a || !tri_b)) || variant < 0 || variant > 2) {
+        snprintf(g_err, sizeof(g_err), "invalid argument");
+        return TC_EINVAL;
+    }
+    if (p->flags & TC_SOA) {
+        snprintf(g_err, sizeof(g_err), "host entry points take the (n,3,3) layout only");
+        return TC_EINVAL;
+    }
+    std::lock_guard<std::mutex> lock(g_host.mu);
+    HostCtx& h = g_host;
+    cudaError_t e;
+    if (!h.init) {
+        for (int k = 0; k < HostCtx::NS; ++k)
+            if ((e = cudaStreamCreateWithFlags(&h.st[k], cudaStreamNonBlocking)) != cudaSuccess)
+                return set_err("cudaStreamCreate", e);
+        if ((e = cudaMalloc(&h.dstats, sizeof(tc_stats))) != cudaSuccess) return set_err("cudaMalloc", e);
+        h.init = true;
+    }
+    const int64_t chunk = 1 << 20;
+    const bool want_ids = (p->flags & TC_EMIT_IDS) && ids;
+    // per-pair bytes staged: inputs, eps, allow, outputs
+    const size_t per = sizeof(T) * (18 + 1 + 11) + 2 + (want_ids ? 4 : 0);
+    const size_t need = per * (size_t)(n < chunk ? (n > 0 ? n : 1) : chunk) + 256 * 16;
+    if (need > h.cap) {
+        for (int k = 0; k < HostCtx::NS; ++k) {
+            if (h.buf[k]) cudaFree(h.buf[k]);
+            h.buf[k] = nullptr;
+            if ((e = cudaMalloc(&h.buf[k], need)) != cudaSuccess) {
+                h.cap = 0;
+                return set_err("cudaMalloc", e);
+            }
+        }
+        h.cap = need;
+    }
+    stats_reset_kernel<<<1, 1, 0, h.st[0]>>>(h.dstats);
+    g_launches++;
+    cudaEvent_t ready;
+    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    cudaEventRecord(ready, h.st[0]);
+    for (int k = 1; k < HostCtx::NS; ++k) cudaStreamWaitEvent(h.st[k], ready, 0);
+    int rc = TC_OK;
+    for (int64_t c0 = 0, ci = 0; c0 < n && rc == TC_OK; c0 += chunk, ++ci) {
+        const int64_t m = (n - c0) < chunk ? (n - c0) : chunk;
+        const int k = (int)(ci % HostCtx::NS);
+        cudaStream_t s = h.st[k];
+        char* base = static_cast<char*>(h.buf[k]);
+        auto carve = [&](size_t bytes) { char* r = base; base += (bytes + 255) & ~size_t(255); return r; };
+        T* dA = (T*)carve(sizeof(T) * 9 * m);
+        T* dB = (T*)carve(sizeof(T) * 9 * m);
+        T* dE = eps ? (T*)carve(sizeof(T) * m) : nullptr;
+        uint8_t* dF = allow ? (uint8_t*)carve(m) : nullptr;
+        T* dD = distance ? (T*)carve(sizeof(T) * m) : nullptr;
+        T* dPA = pa ? (T*)carve(sizeof(T) * 3 * m) : nullptr;
+        T* dPB = pb ? (T*)carve(sizeof(T) * 3 * m) : nullptr;
+        T* dBA = ba ? (T*)carve(sizeof(T) * 2 * m) : nullptr;
+        T* dBB = bb ? (T*)carve(sizeof(T) * 2 * m) : nullptr;
+        int8_t* dK = kind ? (int8_t*)carve(m) : nullptr;
+        uint8_t* dI = want_ids ? (uint8_t*)carve(4 * m) : nullptr;
+        cudaMemcpyAsync(dA, tri_a + 9 * c0, sizeof(T) * 9 * m, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(dB, tri_b + 9 * c0, sizeof(T) * 9 * m, cudaMemcpyHostToDevice, s);
+        if (dE) cudaMemcpyAsync(dE, eps + c0, sizeof(T) * m, cudaMemcpyHostToDevice, s);
+        if (dF) cudaMemcpyAsync(dF, allow + c0, m, cudaMemcpyHostToDevice, s);
+        rc = run_device<T>(variant, dA, dB, m, dE, dF, p, dD, dPA, dPB, dBA, dBB, dK, dI, h.dstats, s);
+        if (dD) cudaMemcpyAsync(distance + c0, dD, sizeof(T) * m, cudaMemcpyDeviceToHost, s);
+        if (dPA) cudaMemcpyAsync(pa + 3 * c0, dPA, sizeof(T) * 3 * m, cudaMemcpyDeviceToHost, s);
+        if (dPB) cudaMemcpyAsync(pb + 3 * c0, dPB, sizeof(T) * 3 * m, cudaMemcpyDeviceToHost, s);
+        if (dBA) cudaMemcpyAsync(ba + 2 * c0, dBA, sizeof(T) * 2 * m, cudaMemcpyDeviceToHost, s);
+        if (dBB) cudaMemcpyAsync(bb + 2 * c0, dBB, sizeof(T) * 2 * m, cudaMemcpyDeviceToHost, s);
+        if (dK) cudaMemcpyAsync(kind + c0, dK, m, cudaMemcpyDeviceToHost, s);
+        if (dI) cudaMemcpyAsync(ids + 4 * c0, dI, 4 * m, cudaMemcpyDeviceToHost, s);
+    }
+    tc_stats hs;
+    for (int k = 1; k < HostCtx::NS; ++k) {
+        cudaEventRecord(ready, h.st[k]);
+        cudaStreamWaitEvent(h.st[0], ready, 0);
+    }
+    cudaMemcpyAsync(&hs, h.dstats, sizeof(tc_stats), cudaMemcpyDeviceToHost, h.st[0]);
+    e = cudaStreamSynchronize(h.st[0]);
+    for (int k = 1; k < HostCtx::NS; ++k) {
+        const cudaError_t e2 = cudaStreamSynchronize(h.st[k]);
+        if (e == cudaSuccess) e = e2;
+    }
+    cudaEventDestroy(ready);
+    if (rc != TC_OK) return rc;
+    if (e != cudaSuccess) return set_err("host pipeline", e);
+    if (stats) {
+        stats->iterative += hs.iterative;
+        stats->comparison += hs.comparison;
+        stats->fallback += hs.fallback;
+        stats->degenerate += hs.degenerate;
+        stats->contacts += hs.contacts;
+        if (hs.min_distance < stats->min_distance) stats->min_distance = hs.min_distance;
+    }
+    if (variant == V_HYBRID && hs.degenerate > 0) {
+        snprintf(g_err, sizeof(g_err), "degenerate triangle in comparison fallback");
+        return TC_EDEGENERATE;
+    }
+    return TC_OK;
+}
+
+template <typename T>
+static int run_cpt(const T* P, const T* Tr, int64_t n, T* closest, T* bary, void* stream) {
+    if (n < 0 || (n > 0 && (!P || !Tr))) return TC_EINVAL;
+    if (n == 0) return TC_OK;
+    auto k = cpt_kernel<T>;
+    k<<<(unsigned)grid_for(k, n), BLOCK, 0, reinterpret_cast<cudaStream_t>(stream)>>>(P, Tr, n, closest, bary);
+    g_launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TC_OK : set_err("cpt launch", e);
+}
+
+template <typename T>
+static int run_degenerate(const T* Tr, int64_t n, uint8_t* mask, void* stream) {
+    if (n < 0 || (n > 0 && (!Tr || !mask))) return TC_EINVAL;
+    if (n == 0) return TC_OK;
+    auto k = degenerate_kernel<T>;
+    k<<<(unsigned)grid_for(k, n), BLOCK, 0, reinterpret_cast<cudaStream_t>(stream)>>>(Tr, n, mask);
+    g_launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TC_OK : set_err("degenerate launch", e);
+}
+
+// Synchronous host-pointer helpers: one temporary device buffer per call.
+template <typename T>
+static int run_cpt_host(const T* P, const T* Tr, int64_t n, T* closest, T* bary) {
+    if (n < 0 || (n > 0 && (!P || !Tr))) return TC_EINVAL;
+    if (n == 0) return TC_OK;
+    char* d = nullptr;
+    const size_t bytes = sizeof(T) * 17 * (size_t)n;
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e != cudaSuccess) return set_err("cudaMalloc", e);
+    T* dP = (T*)d;
+    T* dT = dP + 3 * n;
+    T* dC = dT + 9 * n;
+    T* dB = dC + 3 * n;
+    cudaMemcpy(dP, P, sizeof(T) * 3 * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(dT, Tr, sizeof(T) * 9 * n, cudaMemcpyHostToDevice);
+    int rc = run_cpt<T>(dP, dT, n, dC, dB, nullptr);
+    if (rc == TC_OK) {
+        if (closest) cudaMemcpy(closest, dC, sizeof(T) * 3 * n, cudaMemcpyDeviceToHost);
+        if (bary) cudaMemcpy(bary, dB, sizeof(T) * 2 * n, cudaMemcpyDeviceToHost);
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = set_err("cpt host", e);
+    }
+    cudaFree(d);
+    return rc;
+}
+
+template <typename T>
+static int run_degenerate_host(const T* Tr, int64_t n, uint8_t* mask) {
+    if (n < 0 || (n > 0 && (!Tr || !mask))) return TC_EINVAL;
+    if (n == 0) return TC_OK;
+    char* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(T) * 9 * (size_t)n + (size_t)n);
+    if (e != cudaSuccess) return set_err("cudaMalloc", e);
+    T* dT = (T*)d;
+    uint8_t* dM = (uint8_t*)(dT + 9 * n);
+    cudaMemcpy(dT, Tr, sizeof(T) * 9 * n, cudaMemcpyHostToDevice);
+    int rc = run_degenerate<T>(dT, n, dM, nullptr);
+    if (rc == TC_OK) {
+        cudaMemcpy(mask, dM, n, cudaMemcpyDeviceToHost);
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = set_err("degenerate host", e);
+    }
+    cudaFree(d);
+    return rc;
+}
+
+}  // namespace tc
+
+// ---- C ABI ------------------------------------------------------------------------------
+extern "C" {
+
+void tc_params_default(tc_params* p) {
+    p->epsilon = 1e-2;
+    p->c_factor = 1.0;
+    p->alpha_iterative = 10.0;
+    p->alpha_regulariser = 1e-4;
+    p->move_factor = 0.25;
+    p->start_coord = 1.0 / 3.0;
+    p->n_iterative = 4;
+    p->flags = 0;
+}
+
+int tc_abi_version(void) { return TC_ABI_VERSION; }
+const char* tc_last_error(void) { return tc::g_err; }
+int64_t tc_launch_count(void) { return tc::g_launches.load(); }
+
+int tc_stats_reset(tc_stats* stats, void* stream) {
+    if (!stats) return TC_EINVAL;
+    tc::stats_reset_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(stats);
+    tc::g_launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TC_OK : tc::set_err("stats reset", e);
+}
+
+#define TC_DEVICE_ENTRY(NAME, VARIANT, T)                                                                   \
+    int NAME(const T* tri_a, const T* tri_b, int64_t n, const T* eps, const tc_params* p, T* distance,      \
+             T* point_a, T* point_b, T* bary_a, T* bary_b, int8_t* kind, uint8_t* ids, tc_stats* stats,     \
+             void* stream) {                                                                                \
+        return tc::run_device<T>(VARIANT, tri_a, tri_b, n, eps, nullptr, p, distance, point_a, point_b,    \
+                                 bary_a, bary_b, kind, ids, stats, stream);                                 \
+    }
+TC_DEVICE_ENTRY(tc_comparison_f64, tc::V_COMPARISON, double)
+TC_DEVICE_ENTRY(tc_comparison_f32, tc::V_COMPARISON, float)
+TC_DEVICE_ENTRY(tc_iterative_f64, tc::V_ITERATIVE, double)
+TC_DEVICE_ENTRY(tc_iterative_f32, tc::V_ITERATIVE, float)
+#undef TC_DEVICE_ENTRY
+
+int tc_hybrid_f64(const double* tri_a, const double* tri_b, int64_t n, const double* eps, const uint8_t* allow_fb,
+                  const tc_params* p, double* distance, double* point_a, double* point_b, double* bary_a,
+                  double* bary_b, int8_t* kind, uint8_t* ids, tc_stats* stats, void* stream) {
+    return tc::run_device<double>(tc::V_HYBRID, tri_a, tri_b, n, eps, allow_fb, p, distance, point_a, point_b,
+                                  bary_a, bary_b, kind, ids, stats, stream);
+}
+int tc_hybrid_f32(const float* tri_a, const float* tri_b, int64_t n, const float* eps, const uint8_t* allow_fb,
+                  const tc_params* p, float* distance, float* point_a, float* point_b, float* bary_a,
+                  float* bary_b, int8_t* kind, uint8_t* ids, tc_stats* stats, void* stream) {
+    return tc::run_device<float>(tc::V_HYBRID, tri_a, tri_b, n, eps, allow_fb, p, distance, point_a, point_b,
+                                 bary_a, bary_b, kind, ids, stats, stream);
+}
+
+int tc_closest_point_triangle_f64(const double* points, const double* tris, int64_t n, double* closest,
+                                  double* bary, void* stream) {
+    return tc::run_cpt<double>(points, tris, n, closest, bary, stream);
+}
+int tc_closest_point_triangle_f32(const float* points, const float* tris, int64_t n, float* closest, float* bary,
+                                  void* stream) {
+    return tc::run_cpt<float>(points, tris, n, closest, bary, stream);
+}
+int tc_degenerate_mask_f64(const double* tris, int64_t n, uint8_t* mask, void* stream) {
+    return tc::run_degenerate<double>(tris, n, mask, stream);
+}
+int tc_degenerate_mask_f32(const float* tris, int64_t n, uint8_t* mask, void* stream) {
+    return tc::run_degenerate<float>(tris, n, mask, stream);
+}
+
+int tc_closest_point_triangle_host_f64(const double* points, const double* tris, int64_t n, double* closest,
+                                       double* bary) {
+    return tc::run_cpt_host<double>(points, tris, n, closest, bary);
+}
+int tc_closest_point_triangle_host_f32(const float* points, const float* tris, int64_t n, float* closest,
+                                       float* bary) {
+    return tc::run_cpt_host<float>(points, tris, n, closest, bary);
+}
+int tc_degenerate_mask_host_f64(const double* tris, int64_t n, uint8_t* mask) {
+    return tc::run_degenerate_host<double>(tris, n, mask);
+}
+int tc_degenerate_mask_host_f32(const float* tris, int64_t n, uint8_t* mask) {
+    return tc::run_degenerate_host<float>(tris, n, mask);
+}
+
+int tc_run_host_f64(int variant, const double* tri_a, const double* tri_b, int64_t n, const double* eps,
+                    const uint8_t* allow_fb, const tc_params* p, double* distance, double* point_a,
+                    double* point_b, double* bary_a, double* bary_b, int8_t* kind, uint8_t* ids, tc_stats* stats) {
+    return tc::run_host<double>(variant, tri_a, tri_b, n, eps, allow_fb, p, distance, point_a, point_b, bary_a,
+                                bary_b, kind, ids, stats);
+}
+int tc_run_host_f32(int variant, const float* tri_a, const float* tri_b, int64_t n, const float* eps,
+                    const uint8_t* allow_fb, const tc_params* p, float* distance, float* point_a, float* point_b,
+                    float* bary_a, float* bary_b, int8_t* kind, uint8_t* ids, tc_stats* stats) {
+    return tc::run_host<float>(variant, tri_a, tri_b, n, eps, allow_fb, p, distance, point_a, point_b, bary_a,
+                               bary_b, kind, ids, stats);
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+"""GPU parity: the sm_100a kernels against the reference's golden vectors and
+the CPU oracle, through the C ABI.
+
+* TC_STRICT (device entry points and the drop-in host path): bit-identical
+  to the reference -- every column, kind, ids and counters.
+* fast (FMA-contracted) build: within the north-star tolerance
+  |x - x_ref| <= tau * max(|x_ref|, L), tau = 1e-9 (fp64) / 1e-4 (fp32),
+  L = the pair's longest edge, with kind mismatches allowed only at ties
+  (tests/parity.py).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import DTYPES, PARAM_SETS
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2105_12415_b200 import device as D  # noqa: E402
+from paper_2105_12415_b200 import workloads as W  # noqa: E402
+
+import parity  # noqa: E402
+
+COLS = ("kind", "distance", "point_a", "point_b", "bary_a", "bary_b")
+TDT = {"float64": torch.float64, "float32": torch.float32}
+
+
+def run_dev(variant, A, B, real, pname, strict, soa=False, eps=None, allow=None, ids=True):
+    dt = TDT[real]
+    p = D.Params(**PARAM_SETS[pname])
+    if soa:
+        planes = torch.from_numpy(W.to_soa(A, B)).to("cuda", dt)
+        ta, tb = planes[:9].contiguous(), planes[9:].contiguous()
+    else:
+        ta = torch.from_numpy(np.ascontiguousarray(A)).to("cuda", dt)
+        tb = torch.from_numpy(np.ascontiguousarray(B)).to("cuda", dt)
+    stats = D.new_stats()
+    e = None if eps is None else torch.from_numpy(np.asarray(eps)).to("cuda", dt)
+    al = None if allow is None else torch.from_numpy(np.asarray(allow, np.uint8)).cuda()
+    out = D.run(variant, ta, tb, p, eps=e, allow=al, soa=soa, strict=strict, ids=ids, stats=stats)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    if soa:
+        for k in ("point_a", "point_b", "bary_a", "bary_b"):
+            res[k] = np.ascontiguousarray(res[k].T)
+    return res, D.read_stats(stats)
+
+
+def assert_bitwise(ref, pre, got):
+    for col in COLS:
+        r = ref[f"{pre}_{col}"]
+        g = got[col]
+        neq = ~((r == g) | (np.isnan(r) & np.isnan(g)))
+        assert not neq.any(), f"{pre}.{col}: {int(neq.sum())} differ, rows {np.nonzero(neq)[0][:8]}"
+
+
+@pytest.mark.parametrize("soa", [False, True])
+@pytest.mark.parametrize("real", list(DTYPES))
+@pytest.mark.parametrize("pname", list(PARAM_SETS))
+@pytest.mark.parametrize("case", ["cfg0", "cfg3", "special"])
+def test_strict_bitwise_vs_reference(golden_inputs, golden_ref, case, pname, real, soa):
+    ref = golden_ref[real]
+    dt = DTYPES[real]
+    A = golden_inputs[f"{case}_A"].astype(dt)
+    B = golden_inputs[f"{case}_B"].astype(dt)
+    pre = f"{case}_{pname}"
+    cm, st = run_dev("comparison", A, B, real, pname, True, soa)
+    assert_bitwise(ref, f"{pre}_comparison", cm)
+    assert np.array_equal(cm["ids"], ref[f"{pre}_comparison_ids"])
+    assert st["comparison"] == len(A) and st["fallback"] == 0
+    it, st = run_dev("iterative", A, B, real, pname, True, soa)
+    assert_bitwise(ref, f"{pre}_iterative", it)
+    assert st["iterative"] == len(A)
+    hy, st = run_dev("hybrid", A, B, real, pname, True, soa)
+    if f"{pre}_hybrid_raised" in ref:
+        assert st["degenerate"] > 0
+    else:
+        assert_bitwise(ref, f"{pre}_hybrid", hy)
+        assert [st["iterative"], st["comparison"], st["fallback"]] == list(ref[f"{pre}_hybrid_counters"])
+        assert st["contacts"] == int((hy["kind"] == 1).sum())
+        assert st["min_distance"] == float(hy["distance"].min())
+
+
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_strict_masked_hybrid(golden_inputs, golden_ref, real):
+    dt = DTYPES[real]
+    A = golden_inputs["cfg0_A"][:1024].astype(dt)
+    B = golden_inputs["cfg0_B"][:1024].astype(dt)
+    hy, st = run_dev("hybrid", A, B, real, "def", True, eps=golden_inputs["mask_eps"].astype(dt),
+                     allow=golden_inputs["mask_allow"])
+    assert_bitwise(golden_ref[real], "masked_hybrid", hy)
+    assert [st["iterative"], st["comparison"], st["fallback"]] == list(golden_ref[real]["masked_hybrid_counters"])
+
+
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_point_triangle_and_degenerate(golden_inputs, golden_ref, real):
+    dt = TDT[real]
+    P = torch.from_numpy(golden_inputs["cpt_P"]).to("cuda", dt)
+    T = torch.from_numpy(golden_inputs["cpt_T"]).to("cuda", dt)
+    cl, ba = D.closest_point_triangle(P, T)
+    assert np.array_equal(cl.cpu().numpy(), golden_ref[real]["cpt_closest"])
+    assert np.array_equal(ba.cpu().numpy(), golden_ref[real]["cpt_bary"])
+    m = D.degenerate_mask(torch.from_numpy(golden_inputs["degenerate_T"]).to("cuda", dt))
+    assert np.array_equal(m.cpu().numpy(), golden_ref[real]["degenerate_mask"])
+
+
+@pytest.mark.parametrize("real", list(DTYPES))
+@pytest.mark.parametrize("pname", list(PARAM_SETS))
+@pytest.mark.parametrize("case", ["cfg0", "cfg3"])
+def test_fast_within_tolerance(oracle_lib, golden_inputs, case, pname, real):
+    dt = DTYPES[real]
+    A = golden_inputs[f"{case}_A"].astype(dt)
+    B = golden_inputs[f"{case}_B"].astype(dt)
+    for variant in ("comparison", "iterative", "hybrid"):
+        got, _ = run_dev(variant, A, B, real, pname, False)
+        rep = parity.compare_fast(oracle_lib, variant, A, B, PARAM_SETS[pname], got, dt)
+        assert rep["ok"], rep
+
+
+@pytest.mark.parametrize("n", [1, 31, 255, 256, 257, 4097])
+def test_ragged_sizes_strict(oracle_lib, golden_inputs, n):
+    A = golden_inputs["cfg0_A"][:n]
+    B = golden_inputs["cfg0_B"][:n]
+    p = PARAM_SETS["bl"]
+    hy, st = run_dev("hybrid", A, B, "float64", "bl", True)
+    o, counts, _ = oracle_lib.hybrid(A, B, oracle_lib.make_params(**p), p["epsilon"])
+    for col in COLS:
+        assert np.array_equal(hy[col], o[col]), col
+    assert np.array_equal(hy["ids"], o["ids"])
+    assert [st["iterative"], st["comparison"], st["fallback"]] == list(counts[:3])
+
+
+def test_empty_batch():
+    t = torch.empty((0, 3, 3), dtype=torch.float64, device="cuda")
+    out = D.run("hybrid", t, t, D.Params())
+    assert out["kind"].numel() == 0
+
+
+def test_degenerate_fallback_marks_pairs():
+    """RK/kernels.py:598-600: degenerate triangles only matter on fallback."""
+    U = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float)
+    bad = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float)
+    crawler = U + [40.0, 0, 0.01]
+    far = U + [0, 0, 1.0]
+    A = np.stack([bad, bad, U])
+    B = np.stack([far, crawler, far])
+    hy, st = run_dev("hybrid", A, B, "float64", "def", True)
+    assert hy["kind"][0] != 2                     # settled: never consults the comparison kernel
+    assert hy["kind"][2] == 0
+    if hy["kind"][1] == 3:
+        assert st["degenerate"] == 1
+    assert not (hy["kind"] == 2).any()
