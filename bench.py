@@ -1,0 +1,384 @@
+"""Benchmark of the hybrid fp64 triangle-pair contact kernel (BASELINE.json).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Workload (config 1 of BASELINE.json): 16,777,216 = 2^24 random triangle
+pairs per GPU from the chunked cfg0 generator (seed 0, separation
+U[-0.1, 0.5]), fp64, planar SoA layout [18][n] resident in HBM, hybrid
+kernel at (16 sweeps, eps 1e-6), full result record written.  A step is one
+pass of the hot path over the batch: stats reset, the hybrid kernel, and
+(N > 1) the NCCL all-reduce of the stats record.  Rank r of N works on
+pairs [r*2^24, (r+1)*2^24) of the same generator (weak scaling).  Inputs
+(2.4 GB) and outputs (1.5 GB) exceed the 126 MB L2, so no flush is needed.
+
+``e2e`` times the same workload through the reference-facing C-ABI host
+entry point tc_run_host_f64 (the call the drop-in ``tricontact.kernels``
+makes) with pinned host buffers in the reference's (n,3,3) layout: H2D of
+the inputs, kernel and D2H of the full result record are inside its timed
+region.
+
+``--impl reference`` times the reference's CPU path -- the oracle port
+(oracle/tc_oracle.c: the reference is pure numpy and cannot travel to the
+GPU box) -- with every host thread, on bounded samples of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+N_PAIRS = 1 << 24
+PARAMS = dict(n_iterative=16, epsilon=1e-6)
+SEP = (-0.1, 0.5)
+METRIC = "triangle-pair contact queries/sec (hybrid, fp64)"
+UNIT = "pairs/s"
+
+
+def flops_per_launch(n, n_it, fallback, intersecting):
+    """200 + 88 N per pair, +1199 per fallback, +254 if it intersects."""
+    return n * (200 + 88 * n_it) + 1199 * fallback + 254 * intersecting
+
+
+# ---------------------------------------------------------------------------
+# clocks: nvidia-smi sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), float(parts[2]), parts[4:8]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        maxclk = max(r[1] for r in rows)
+        load = [r for r in rows if r[2] > 200.0] or rows
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": maxclk, "reasons": reasons,
+                "samples": len(load), "power_w_max": max(r[2] for r in rows)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_oracle_rate(seconds: float, chunk: int, threads: int, start: int = 0):
+    """Time the oracle port's hybrid on consecutive chunks until `seconds` pass."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+    from paper_2105_12415_b200 import workloads as W
+    p = oracle.make_params(**PARAMS)
+    done, elapsed, k = 0, 0.0, 0
+    while elapsed < seconds:
+        A, B = W.random_pairs(chunk, seed=0, sep=SEP, start=start + k * chunk)
+        t0 = time.perf_counter()
+        _, _, rc = oracle.hybrid(A, B, p, PARAMS["epsilon"], threads=threads)
+        elapsed += time.perf_counter() - t0
+        assert rc == 0
+        done += chunk
+        k += 1
+    return done / elapsed, done
+
+
+def run_reference(args, rank):
+    """--impl reference: the CPU path on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+    from paper_2105_12415_b200 import workloads as W
+    oracle.build()
+    sample = 1 << 16
+    p = oracle.make_params(**PARAMS)
+    A, B = W.random_pairs(sample, seed=0, sep=SEP)
+    for _ in range(args.warmup):
+        oracle.hybrid(A, B, p, PARAMS["epsilon"], threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, _, rc = oracle.hybrid(A, B, p, PARAMS["epsilon"], threads=threads)
+        assert rc == 0
+    dt = time.perf_counter() - t0
+    value = sample * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded cfg0 generator)",
+        "config": {"workload": "cfg1: hybrid fp64, 16 sweeps, eps 1e-6, random pairs sep U[-0.1,0.5]",
+                   "pairs_per_step": sample, "layout": "(n,3,3) host"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} pairs of the cfg1 generator per step (oracle/tc_oracle.c, "
+                                   "C restatement of RK/kernels.py, bit-identical to the reference)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_PAIRS, help="pairs per GPU")
+    ap.add_argument("--strict", action="store_true", help="time the bit-exact TC_STRICT build")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu baseline / variant table")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2105_12415_b200 import _abi, device as D, shard, workloads as W
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = _abi.load()
+    n = args.n
+
+    # ---- inputs: this rank's range of the cfg1 generator, SoA planes in HBM
+    A, B = W.random_pairs(n, seed=0, sep=SEP, start=rank * n)
+    planes = torch.from_numpy(W.to_soa(A, B)).to(dev)
+    ta, tb = planes[:9], planes[9:]
+    out = D.alloc_outputs(n, torch.float64, dev, soa=True)
+    stats = D.new_stats(dev)
+    params = D.Params(**PARAMS)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        D.reset_stats(stats)
+        if ev is not None:
+            ev[0].record(stream)
+        D.run("hybrid", ta, tb, params, soa=True, strict=args.strict, out=out, stats=stats, n=n)
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:
+            shard.allreduce_stats(stats)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = D.launch_count()
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(kev[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = D.launch_count() - launches0
+    ms_total = t_start.elapsed_time(t_end)
+    ms_kernel = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    t = torch.tensor([ms_total, ms_kernel], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total, ms_kernel = float(t[0]), float(t[1])
+    ms_step = ms_total / args.steps
+    st = shard.stats_dict(stats)  # after the last step's all-reduce: whole-job tallies
+    value = n * world / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (hybrid_kernel): FP64 pipe
+    n_local = n
+    fb_local = st["fallback"] / world
+    fbx_local = st["intersecting"] / world
+    flops = flops_per_launch(n_local, PARAMS["n_iterative"], fb_local, fbx_local)
+    achieved_tf = flops / (ms_kernel / 1e3) / 1e12
+    sink = torch.empty(4096, dtype=torch.float64, device=dev)
+    blocks = 148 * 8
+    lib.tc_fma_probe(1, blocks, 64, ctypes.c_void_p(sink.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(5):
+        e0.record(stream)
+        fl = lib.tc_fma_probe(1, blocks, 2048, ctypes.c_void_p(sink.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        best = max(best, fl / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    peak_tf = best
+    bytes_per_pair = 144 + 89  # SoA inputs + full result record
+    hbm_gbs = n_local * bytes_per_pair / (ms_kernel / 1e3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_hybrid_f64_summary.json"
+    if prof.exists():
+        try:
+            pj = json.loads(prof.read_text())
+            if pj.get("n") == n_local:
+                traffic = pj.get("dram_bytes_per_launch")
+        except ValueError:
+            pass
+    roofline = {
+        "bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
+        "traffic": traffic,
+        "kernel": "hybrid_kernel<double,fast,soa>", "kernel_ms": ms_kernel,
+        "flops_per_launch": flops, "flop_model": "SURVEY.md App. A: n(200+88N) + 1199 fallback + 254 fallback&intersect",
+        "peak_source": "in-run DFMA probe (tc_fma_probe); MEASURED_PEAKS.json has no FP64 figure",
+        "hbm": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
+                "bytes_per_pair": bytes_per_pair, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+    }
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg0/cfg1 generator, SURVEY.md 8d)",
+        "config": {"workload": "cfg1: 2^24 random triangle pairs per GPU, hybrid fp64, 16 sweeps, eps 1e-6",
+                   "pairs_per_gpu": n, "layout": "SoA [18][n] in HBM", "rounding": "strict" if args.strict else "fast",
+                   "l2": "inputs 2.4 GB + outputs 1.5 GB per GPU > 126 MB L2 (no flush needed)",
+                   "parallelism": f"dp{world} contiguous shards + NCCL all-reduce of stats" if world > 1 else "1 GPU"},
+        "roofline": roofline,
+        "gpu_launches": launches,
+        "stats": st,
+        "fallback_rate": st["fallback"] / (n * world),
+    }
+
+    clocks = clk.summary()
+    line["clocks"] = clocks
+
+    if not args.no_extras:
+        # ---- e2e through the host C-ABI entry point (pinned host buffers)
+        line["e2e"] = e2e_measure(lib, _abi, torch, A, B, n, world, dist, dev)
+        if rank == 0 and world == 1:
+            threads = len(os.sched_getaffinity(0))
+            rate, done = cpu_oracle_rate(10.0, 1 << 17, threads)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                    "sample": f"{done} pairs of the cfg1 generator in 131072-pair chunks, hybrid "
+                                              "(16, 1e-6), oracle/tc_oracle.c on all host threads"}
+            line["variants"] = variant_table(D, torch, A[: 1 << 22], B[: 1 << 22], dev)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_measure(lib, _abi, torch, A, B, n, world, dist, dev, reps=3):
+    """Hybrid through tc_run_host_f64 with pinned host buffers (reference layout)."""
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True)
+    hA = pin((n, 3, 3), torch.float64)
+    hB = pin((n, 3, 3), torch.float64)
+    hA.numpy()[:] = A
+    hB.numpy()[:] = B
+    outs = {"distance": pin((n,), torch.float64), "point_a": pin((n, 3), torch.float64),
+            "point_b": pin((n, 3), torch.float64), "bary_a": pin((n, 2), torch.float64),
+            "bary_b": pin((n, 2), torch.float64), "kind": pin((n,), torch.int8)}
+    from paper_2105_12415_b200 import device as D
+    p = _abi.params_struct(D.Params(**PARAMS), 0)
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr())
+    stats = _abi.TcStats(0, 0, 0, 0, 0, 0, float("inf"))
+
+    def call():
+        rc = lib.tc_run_host_f64(2, ptr(hA), ptr(hB), n, None, None, ctypes.byref(p), ptr(outs["distance"]),
+                                 ptr(outs["point_a"]), ptr(outs["point_b"]), ptr(outs["bary_a"]),
+                                 ptr(outs["bary_b"]), ptr(outs["kind"]), None, ctypes.byref(stats))
+        _abi.check(rc, "tc_run_host_f64")
+
+    call()
+    times = []
+    for _ in range(reps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t[0])
+    return {"value": n * world / sec, "unit": UNIT, "h2d_bytes_per_step": n * 144 * world,
+            "d2h_bytes_per_step": n * 89 * world, "ms_per_step": 1e3 * sec,
+            "path": "tc_run_host_f64 (host C ABI, pinned, 1M-pair chunks on 3 streams)"}
+
+
+def variant_table(D, torch, A, B, dev, reps=3):
+    """Kernel-only rates of every variant x dtype x rounding on 2^22 pairs (SoA, full record)."""
+    from paper_2105_12415_b200 import workloads as W
+    res = {}
+    n = A.shape[0]
+    P = D.Params(**PARAMS)
+    for dt, name in ((torch.float64, "f64"), (torch.float32, "f32")):
+        planes = torch.from_numpy(W.to_soa(A, B)).to(dev, dt)
+        ta, tb = planes[:9], planes[9:]
+        out = D.alloc_outputs(n, dt, dev, soa=True)
+        for variant in ("iterative", "comparison", "hybrid"):
+            for strict in (False, True):
+                D.run(variant, ta, tb, P, soa=True, strict=strict, out=out, n=n)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    D.run(variant, ta, tb, P, soa=True, strict=strict, out=out, n=n)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                res[f"{variant}_{name}_{'strict' if strict else 'fast'}"] = round(n / (ms / 1e3), 1)
+    res["unit"] = "pairs/s, 2^22 pairs, SoA, full record, (16, 1e-6)"
+    return res
+
+
+if __name__ == "__main__":
+    main()

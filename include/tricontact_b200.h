@@ -77,6 +77,7 @@ typedef struct {
     int64_t fallback;     /* fallback_invocations */
     int64_t degenerate;   /* fallback pairs with a degenerate triangle */
     int64_t contacts;     /* pairs whose final kind is CONTACT */
+    int64_t intersecting; /* comparison results that found a proper edge-face crossing */
     double min_distance;  /* min final distance over non-degenerate pairs (+inf if none) */
 } tc_stats;
 
@@ -158,6 +159,12 @@ int tc_closest_point_triangle_host_f32(const float* points, const float* tris, i
                                        float* closest, float* bary);
 int tc_degenerate_mask_host_f64(const double* tris, int64_t n, uint8_t* mask);
 int tc_degenerate_mask_host_f32(const float* tris, int64_t n, uint8_t* mask);
+
+/* FMA-pipe throughput probe (fp64 != 0: DFMA, else FFMA): enqueues one launch
+ * of `blocks` CTAs and returns its flop count (or -1); time it with events
+ * to get the FP64/FP32 roofline denominator.  sink: device scratch, >= blocks
+ * elements. */
+int64_t tc_fma_probe(int fp64, int64_t blocks, int iters, void* sink, void* stream);
 
 /* Number of kernel launches this library has enqueued since load. */
 int64_t tc_launch_count(void);

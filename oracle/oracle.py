@@ -44,10 +44,23 @@ class OracleParams(ctypes.Structure):
 
 def build(force: bool = False) -> Path:
     """Compile the oracle with its Makefile (gcc, -ffp-contract=off)."""
-    if force or not _LIB_PATH.exists() or _LIB_PATH.stat().st_mtime < max(
+    if force or not _LIB_PATH.exists() or not (_HERE / "libtc_oracle_fma.so").exists() or _LIB_PATH.stat().st_mtime < max(
             p.stat().st_mtime for p in _HERE.glob("tc_oracle*")):
         subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
     return _LIB_PATH
+
+
+def fma_variant():
+    """A second copy of this module bound to libtc_oracle_fma.so (FMA-contracted
+    build of the same restatement; CPU stand-in for the GPU fast build)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("oracle_fma", __file__)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod._LIB_PATH = _HERE / "libtc_oracle_fma.so"
+    if not mod._LIB_PATH.exists():
+        build(force=True)
+    return mod
 
 
 def lib():
@@ -65,7 +78,8 @@ def lib():
             getattr(_lib, f"tco_hybrid_{sfx}").argtypes = [p, p, i64, p, p, p] + [p] * 8 + [i32]
             getattr(_lib, f"tco_closest_point_triangle_{sfx}").argtypes = [p, p, i64, p, p, i32]
             getattr(_lib, f"tco_degenerate_{sfx}").argtypes = [p, i64, p, i32]
-            for name in ("comparison", "iterative", "hybrid", "closest_point_triangle", "degenerate"):
+            getattr(_lib, f"tco_margins_{sfx}").argtypes = [p, p, i64, p, p, p, i32]
+            for name in ("comparison", "iterative", "hybrid", "closest_point_triangle", "degenerate", "margins"):
                 getattr(_lib, f"tco_{name}_{sfx}").restype = ctypes.c_int
     return _lib
 
@@ -180,3 +194,15 @@ def degenerate(T, dtype=np.float64, threads=1):
     rc = getattr(lib(), f"tco_degenerate_{_sfx(dtype)}")(_ptr(T), T.shape[0], _ptr(m), threads)
     assert rc == 0
     return m.astype(bool)
+
+
+def margins(A, B, params, eps, dtype=np.float64, threads=1):
+    """(n, 10) float64 decision margins (layout in tc_oracle_impl.h, tco_margins_*)."""
+    A = _tris(A, dtype); B = _tris(B, dtype)
+    n = A.shape[0]
+    e = _eps(eps, n, dtype)
+    m = np.empty((n, 10), np.float64)
+    rc = getattr(lib(), f"tco_margins_{_sfx(dtype)}")(_ptr(A), _ptr(B), n, _ptr(e), ctypes.byref(params), _ptr(m),
+                                                     threads)
+    assert rc == 0
+    return m

@@ -27,6 +27,8 @@ typedef struct {
     int32_t flags;
 } tco_params;
 
+#define TCO_N_MARGINS 10
+
 /* Result columns (RK/kernels.py:96-105): any pointer may be NULL.
  * ids: 4 bytes per pair (see oracle/README.md); NULL to skip. */
 #define TCO_DECL(SFX, REAL)                                                              \
@@ -43,7 +45,9 @@ typedef struct {
                          int8_t* kind, uint8_t* ids, int64_t* counts, int threads);      \
     int tco_closest_point_triangle_##SFX(const REAL* P, const REAL* T, int64_t n,        \
                                          REAL* closest, REAL* bary, int threads);        \
-    int tco_degenerate_##SFX(const REAL* T, int64_t n, uint8_t* mask, int threads);
+    int tco_degenerate_##SFX(const REAL* T, int64_t n, uint8_t* mask, int threads);              \
+    int tco_margins_##SFX(const REAL* A, const REAL* B, int64_t n, const REAL* eps,              \
+                          const tco_params* p, double* margins, int threads);
 
 TCO_DECL(f64, double)
 TCO_DECL(f32, float)

@@ -49,6 +49,14 @@ static inline REAL FN(clip_)(REAL x, REAL lo, REAL hi) {
 /* np.maximum(a, b) for non-NaN input. */
 static inline REAL FN(max_)(REAL a, REAL b) { return (a >= b) ? a : b; }
 
+/* Decision margins of the last helper call on this thread (test-side tie
+ * classification of the FMA build, tests/parity.py); they do not feed back
+ * into any result. */
+static __thread double FN(tl_pt_d_), FN(tl_pt_v_), FN(tl_seg_), FN(tl_cx_plane_), FN(tl_cx_inside_);
+
+static inline double FN(fabsd_)(double x) { return x < 0 ? -x : x; }
+static inline double FN(mind_)(double a, double b) { return a < b ? a : b; }
+
 /* RK/geometry.py:68-75 degenerate_mask (rel_tol = 1e-12). */
 static int FN(degenerate_one_)(const REAL* t) {
     REAL e1[3], e2[3], c[3], ed[3];
@@ -91,6 +99,15 @@ static int FN(closest_point_triangle_one_)(const REAL* p, const REAL* tri, REAL*
     t1 = d1 * d4; t2 = d3 * d2; REAL vc = t1 - t2;
     t1 = d5 * d2; t2 = d1 * d6; REAL vb = t1 - t2;
     t1 = d3 * d6; t2 = d5 * d4; REAL va = t1 - t2;
+    {
+        double m = FN(fabsd_)(d1);
+        m = FN(mind_)(m, FN(fabsd_)(d2)); m = FN(mind_)(m, FN(fabsd_)(d3));
+        m = FN(mind_)(m, FN(fabsd_)(d4)); m = FN(mind_)(m, FN(fabsd_)(d5));
+        m = FN(mind_)(m, FN(fabsd_)(d6)); m = FN(mind_)(m, FN(fabsd_)((double)d4 - d3));
+        m = FN(mind_)(m, FN(fabsd_)((double)d5 - d6));
+        FN(tl_pt_d_) = m;
+        FN(tl_pt_v_) = FN(mind_)(FN(mind_)(FN(fabsd_)(va), FN(fabsd_)(vb)), FN(fabsd_)(vc));
+    }
     REAL u = 0, w = 0;
     int region;
     if (d1 <= 0 && d2 <= 0) {
@@ -154,12 +171,15 @@ static int FN(segment_segment_)(const REAL* p1, const REAL* q1, const REAL* p2, 
     REAL denom = t1 - t2;
     int code = 0;
     REAL s;
+    double sm = 1e300;
     if (denom > TC_TINY_) {
         code |= 1;
         t1 = b * f;
         t2 = c * e;
         REAL num = t1 - t2;
-        s = FN(clip_)(num / denom, 0, 1);
+        REAL sr = num / denom;
+        sm = FN(mind_)(FN(fabsd_)(sr), FN(fabsd_)((double)sr - 1));
+        s = FN(clip_)(sr, 0, 1);
     } else {
         s = 0;
     }
@@ -167,15 +187,21 @@ static int FN(segment_segment_)(const REAL* p1, const REAL* q1, const REAL* p2, 
     REAL t = b * s;
     t = t + f;
     t = t / e_safe;
+    sm = FN(mind_)(sm, FN(mind_)(FN(fabsd_)(t), FN(fabsd_)((double)t - 1)));
     REAL a_safe = (a > TC_TINY_) ? a : (REAL)1;
     if (t < 0) {
         code |= 2;
-        s = FN(clip_)((-c) / a_safe, 0, 1);
+        REAL sr = (-c) / a_safe;
+        sm = FN(mind_)(sm, FN(mind_)(FN(fabsd_)(sr), FN(fabsd_)((double)sr - 1)));
+        s = FN(clip_)(sr, 0, 1);
     } else if (t > 1) {
         code |= 4;
         REAL bc = b - c;
-        s = FN(clip_)(bc / a_safe, 0, 1);
+        REAL sr = bc / a_safe;
+        sm = FN(mind_)(sm, FN(mind_)(FN(fabsd_)(sr), FN(fabsd_)((double)sr - 1)));
+        s = FN(clip_)(sr, 0, 1);
     }
+    FN(tl_seg_) = sm;
     t = FN(clip_)(t, 0, 1);
     for (int i = 0; i < 3; ++i) {
         REAL x = s * d1[i];
@@ -224,6 +250,12 @@ static int FN(segment_triangle_crossing_)(const REAL* p, const REAL* q, const RE
     REAL b2 = (t1 - t2) / det_safe;
     REAL bs = b1 + b2;
     int inside = (b1 >= 0) && (b2 >= 0) && (bs <= 1);
+    {
+        double nn = sqrt((double)nrm[0] * nrm[0] + (double)nrm[1] * nrm[1] + (double)nrm[2] * nrm[2]);
+        FN(tl_cx_plane_) = nn > 0 ? FN(mind_)(FN(fabsd_)(dp), FN(fabsd_)(dq)) / nn : 0;
+        FN(tl_cx_inside_) = crossing ? FN(mind_)(FN(mind_)(FN(fabsd_)(b1), FN(fabsd_)(b2)),
+                                                 FN(fabsd_)(1.0 - (double)b1 - b2)) : 1e300;
+    }
     return crossing && inside;
 }
 
@@ -240,12 +272,30 @@ typedef struct {
     REAL distance, pa[3], pb[3], ba[2], bb[2];
     int8_t kind;
     uint8_t ids[4];
+    double mg[10]; /* decision margins, see tco_margins_* */
 } FN(rec_);
 
 /* RK/kernels.py:301-401 comparison_batch, one pair. */
 static void FN(comparison_one_)(const REAL* A, const REAL* B, REAL eps, FN(rec_)* out) {
     REAL best = 0, pa[3], pb[3], ba[2], bb[2];
     int best_row = -1, best_code = 0;
+    double second = 1e300, win_margin = 1e300;
+    /* squared scale of the pair, to normalise region-test operands */
+    double sq = 0;
+    {
+        double m = 0;
+        for (int t = 0; t < 2; ++t) {
+            const REAL* T = t ? B : A;
+            for (int k = 0; k < 3; ++k) {
+                const REAL* p0 = T + 3 * k;
+                const REAL* p1 = T + 3 * ((k + 1) % 3);
+                double e = 0;
+                for (int i = 0; i < 3; ++i) e += ((double)p1[i] - p0[i]) * ((double)p1[i] - p0[i]);
+                m = e > m ? e : m;
+            }
+        }
+        sq = m > 0 ? m : 1;
+    }
     int row = 0;
     REAL closest[3], diff[3], u, w, d2;
     for (int k = 0; k < 3; ++k, ++row) {
@@ -253,8 +303,11 @@ static void FN(comparison_one_)(const REAL* A, const REAL* B, REAL eps, FN(rec_)
         int reg = FN(closest_point_triangle_one_)(pt, B, closest, &u, &w);
         FN(sub3_)(pt, closest, diff);
         d2 = FN(dot3_)(diff, diff);
+        if (best_row >= 0 && !(d2 < best) && d2 < second) second = d2;
+        double wm = FN(mind_)(FN(tl_pt_d_) / sq, FN(tl_pt_v_) / (sq * sq));
         if (best_row < 0 || d2 < best) {
-            best = d2; best_row = row; best_code = reg;
+            if (best_row >= 0) second = best;
+            best = d2; best_row = row; best_code = reg; win_margin = wm;
             for (int i = 0; i < 3; ++i) { pa[i] = pt[i]; pb[i] = closest[i]; }
             ba[0] = (k == 1) ? 1 : 0; ba[1] = (k == 2) ? 1 : 0;
             bb[0] = u; bb[1] = w;
@@ -265,8 +318,11 @@ static void FN(comparison_one_)(const REAL* A, const REAL* B, REAL eps, FN(rec_)
         int reg = FN(closest_point_triangle_one_)(pt, A, closest, &u, &w);
         FN(sub3_)(pt, closest, diff);
         d2 = FN(dot3_)(diff, diff);
+        if (best_row >= 0 && !(d2 < best) && d2 < second) second = d2;
+        double wm = FN(mind_)(FN(tl_pt_d_) / sq, FN(tl_pt_v_) / (sq * sq));
         if (d2 < best) {
-            best = d2; best_row = row; best_code = reg;
+            second = best;
+            best = d2; best_row = row; best_code = reg; win_margin = wm;
             for (int i = 0; i < 3; ++i) { pa[i] = closest[i]; pb[i] = pt[i]; }
             ba[0] = u; ba[1] = w;
             bb[0] = (k == 1) ? 1 : 0; bb[1] = (k == 2) ? 1 : 0;
@@ -280,8 +336,11 @@ static void FN(comparison_one_)(const REAL* A, const REAL* B, REAL eps, FN(rec_)
                                             &s, &t, c1, c2);
             FN(sub3_)(c1, c2, diff);
             d2 = FN(dot3_)(diff, diff);
+            if (!(d2 < best) && d2 < second) second = d2;
+            double wm = FN(tl_seg_);
             if (d2 < best) {
-                best = d2; best_row = row; best_code = code;
+                second = best;
+                best = d2; best_row = row; best_code = code; win_margin = wm;
                 for (int i = 0; i < 3; ++i) { pa[i] = c1[i]; pb[i] = c2[i]; }
                 FN(edge_bary_)(ka, s, ba);
                 FN(edge_bary_)(kb, t, bb);
@@ -292,9 +351,12 @@ static void FN(comparison_one_)(const REAL* A, const REAL* B, REAL eps, FN(rec_)
     /* six edge-to-plane tests */
     REAL pts[6][3];
     int ok[6], any = 0;
+    double cx_plane = 1e300, cx_inside = 1e300;
     for (int k = 0; k < 3; ++k) {
         ok[k] = FN(segment_triangle_crossing_)(A + 3 * FN(EDGE_START_)[k], A + 3 * FN(EDGE_END_)[k], B, pts[k]);
+        cx_plane = FN(mind_)(cx_plane, FN(tl_cx_plane_)); cx_inside = FN(mind_)(cx_inside, FN(tl_cx_inside_));
         ok[k + 3] = FN(segment_triangle_crossing_)(B + 3 * FN(EDGE_START_)[k], B + 3 * FN(EDGE_END_)[k], A, pts[k + 3]);
+        cx_plane = FN(mind_)(cx_plane, FN(tl_cx_plane_)); cx_inside = FN(mind_)(cx_inside, FN(tl_cx_inside_));
         any |= ok[k] | ok[k + 3];
     }
     uint8_t pair_id = 255;
@@ -335,6 +397,13 @@ static void FN(comparison_one_)(const REAL* A, const REAL* B, REAL eps, FN(rec_)
     out->ids[1] = (uint8_t)best_code;
     out->ids[2] = pair_id;
     out->ids[3] = any ? 16 : 0;
+    out->mg[0] = second - (double)best;
+    out->mg[1] = (double)distance - (double)thr;
+    out->mg[2] = cx_plane;
+    out->mg[3] = cx_inside;
+    out->mg[7] = win_margin;
+    out->mg[8] = (double)SQRT(best);
+    out->mg[9] = 0;
 }
 
 /* RK/kernels.py:417-431 _penalty_value, summed left to right. */
@@ -481,6 +550,9 @@ static void FN(iterative_one_)(const REAL* A, const REAL* B, REAL eps, const tco
     out->bb[0] = x[2]; out->bb[1] = x[3];
     out->ids[0] = 255; out->ids[1] = 255; out->ids[2] = 255;
     out->ids[3] = (uint8_t)((settled ? 1 : 0) | (contact ? 2 : 0));
+    out->mg[4] = (double)dj - (double)ceps;
+    out->mg[5] = (double)move - (double)meps;
+    out->mg[6] = (double)jh - (double)thr;
 }
 
 static inline void FN(store_)(const FN(rec_)* r, int64_t i, REAL* distance, REAL* point_a,
@@ -555,6 +627,18 @@ static void FN(hybrid_body_)(int64_t lo, int64_t hi, int tid, void* arg) {
     c->n_deg[tid] += n_deg;
 }
 
+static void FN(margins_body_)(int64_t lo, int64_t hi, int tid, void* arg) {
+    FN(ctx_)* c = (FN(ctx_)*)arg;
+    (void)tid;
+    double* mg = (double*)c->distance;
+    for (int64_t i = lo; i < hi; ++i) {
+        FN(rec_) rc, ri;
+        FN(comparison_one_)(c->A + 9 * i, c->B + 9 * i, c->eps[i], &rc);
+        FN(iterative_one_)(c->A + 9 * i, c->B + 9 * i, c->eps[i], c->p, &ri);
+        for (int k = 0; k < TCO_N_MARGINS; ++k) mg[TCO_N_MARGINS * i + k] = (k >= 4 && k <= 6) ? ri.mg[k] : rc.mg[k];
+    }
+}
+
 static void FN(cpt_body_)(int64_t lo, int64_t hi, int tid, void* arg) {
     FN(ctx_)* c = (FN(ctx_)*)arg;
     (void)tid;
@@ -617,6 +701,23 @@ int FN(tco_hybrid_)(const REAL* A, const REAL* B, int64_t n, const REAL* eps,
         counts[3] += n_deg;
     }
     return n_deg ? 2 : 0;
+}
+
+/* Decision margins per pair (TCO_N_MARGINS = 10 doubles): [0] second-best minus best squared
+ * feature distance, [1] distance - 2 eps, [2] min endpoint-to-plane distance
+ * of the six crossing tests, [3] min barycentric inside margin of the tests
+ * whose endpoints straddle the plane, [4] |dJ| - c eps, [5] move - mf eps,
+ * [6] J_hat - 2 eps^2, [7] normalised region / segment-branch margin of the
+ * winning feature, [8] the feature distance before the crossing override
+ * (the answer had no crossing been found), [9] reserved.  Test-side tie
+ * classification only. */
+int FN(tco_margins_)(const REAL* A, const REAL* B, int64_t n, const REAL* eps, const tco_params* p,
+                     double* margins, int threads) {
+    if (n < 0 || !p || (n > 0 && (!A || !B || !eps || !margins))) return 1;
+    FN(ctx_) c = {0};
+    c.A = A; c.B = B; c.eps = eps; c.p = p; c.distance = (REAL*)margins;
+    tco_parallel_for(n, threads, FN(margins_body_), &c);
+    return 0;
 }
 
 int FN(tco_closest_point_triangle_)(const REAL* P, const REAL* T, int64_t n, REAL* closest,

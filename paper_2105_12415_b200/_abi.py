@@ -38,6 +38,7 @@ class TcStats(ctypes.Structure):
         ("fallback", ctypes.c_int64),
         ("degenerate", ctypes.c_int64),
         ("contacts", ctypes.c_int64),
+        ("intersecting", ctypes.c_int64),
         ("min_distance", ctypes.c_double),
     ]
 
@@ -56,6 +57,7 @@ SIGNATURES = {
     "tc_last_error": (ctypes.c_char_p, []),
     "tc_launch_count": (_I64, []),
     "tc_stats_reset": (_INT, [_P, _P]),
+    "tc_fma_probe": (_I64, [_INT, _I64, _INT, _P, _P]),
     "tc_closest_point_triangle_f64": (_INT, [_P, _P, _I64, _P, _P, _P]),
     "tc_closest_point_triangle_f32": (_INT, [_P, _P, _I64, _P, _P, _P]),
     "tc_degenerate_mask_f64": (_INT, [_P, _I64, _P, _P]),

@@ -108,13 +108,14 @@ __device__ __forceinline__ void store_rec(const Args<T>& a, int64_t i, const Rec
 
 // ---- per-CTA tallies -> tc_stats ----------------------------------------------
 struct Tally {
-    unsigned long long iterative = 0, comparison = 0, degenerate = 0, contacts = 0;
+    unsigned long long iterative = 0, comparison = 0, degenerate = 0, contacts = 0, intersecting = 0;
     double min_d = __builtin_huge_val();
 
     template <class R>
     __device__ __forceinline__ void result(const Rec<R>& r) {
         if (r.kind == KIND_DEGENERATE) return;
         contacts += (r.kind == KIND_CONTACT);
+        intersecting += (r.ids >> 24) & FLAG_INTERSECT ? 1 : 0;
         const double d = (double)val(r.distance) + 0.0;  // -0 -> +0
         min_d = (d < min_d) ? d : min_d;
     }
@@ -123,7 +124,7 @@ struct Tally {
     template <bool COMPARISON_IS_FALLBACK>
     __device__ void flush(tc_stats* s) {
         if (!s) return;
-        __shared__ unsigned long long red[5][BLOCK / 32];
+        __shared__ unsigned long long red[5][BLOCK / 32];  // iterative, comparison, degenerate, contacts, intersecting
         __shared__ double redm[BLOCK / 32];
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -132,19 +133,21 @@ struct Tally {
             comparison += __shfl_xor_sync(0xffffffffu, comparison, off);
             degenerate += __shfl_xor_sync(0xffffffffu, degenerate, off);
             contacts += __shfl_xor_sync(0xffffffffu, contacts, off);
+            intersecting += __shfl_xor_sync(0xffffffffu, intersecting, off);
             const double o = __shfl_xor_sync(0xffffffffu, min_d, off);
             min_d = (o < min_d) ? o : min_d;
         }
         if (lane == 0) {
             red[0][wid] = iterative; red[1][wid] = comparison; red[2][wid] = degenerate; red[3][wid] = contacts;
+            red[4][wid] = intersecting;
             redm[wid] = min_d;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            unsigned long long v[4] = {0, 0, 0, 0};
+            unsigned long long v[5] = {0, 0, 0, 0, 0};
             double m = __builtin_huge_val();
             for (int w = 0; w < BLOCK / 32; ++w) {
-                for (int k = 0; k < 4; ++k) v[k] += red[k][w];
+                for (int k = 0; k < 5; ++k) v[k] += red[k][w];
                 m = (redm[w] < m) ? redm[w] : m;
             }
             auto* c = reinterpret_cast<unsigned long long*>(s);
@@ -155,6 +158,7 @@ struct Tally {
             }
             if (v[2]) atomicAdd(c + 3, v[2]);
             if (v[3]) atomicAdd(c + 4, v[3]);
+            if (v[4]) atomicAdd(c + 5, v[4]);
             // distances are >= 0 (or NaN, skipped): IEEE order == unsigned bit order
             if (m == m && m < __builtin_huge_val())
                 atomicMin(reinterpret_cast<unsigned long long*>(&s->min_distance),
@@ -307,8 +311,31 @@ __global__ void __launch_bounds__(BLOCK) degenerate_kernel(const T* Tr, int64_t 
     }
 }
 
+// FMA-pipe throughput probe: 8 independent FMA chains per thread, the
+// denominator of the FP64/FP32 roofline (MEASURED_PEAKS.json has no FP64
+// figure).  flops per launch = 2 * 8 * iters * blocks * BLOCK.
+template <typename T>
+__global__ void __launch_bounds__(BLOCK) fma_probe_kernel(T* sink, int iters) {
+    T a[8];
+    const T b = T(0.999999), c = T(1e-7);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = T(threadIdx.x + k) * T(1e-3);
+#pragma unroll 1
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
+        }
+    }
+    T s = T(0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += a[k];
+    if (s == T(-1)) sink[blockIdx.x] = s;  // never true; keeps the chains alive
+}
+
 __global__ void stats_reset_kernel(tc_stats* s) {
-    s->iterative = s->comparison = s->fallback = s->degenerate = s->contacts = 0;
+    s->iterative = s->comparison = s->fallback = s->degenerate = s->contacts = s->intersecting = 0;
     s->min_distance = __builtin_huge_val();
 }
 
@@ -494,6 +521,7 @@ static int run_host(int variant, const T* tri_a, const T* tri_b, int64_t n, cons
         stats->fallback += hs.fallback;
         stats->degenerate += hs.degenerate;
         stats->contacts += hs.contacts;
+        stats->intersecting += hs.intersecting;
         if (hs.min_distance < stats->min_distance) stats->min_distance = hs.min_distance;
     }
     if (variant == V_HYBRID && hs.degenerate > 0) {
@@ -590,6 +618,16 @@ void tc_params_default(tc_params* p) {
 int tc_abi_version(void) { return TC_ABI_VERSION; }
 const char* tc_last_error(void) { return tc::g_err; }
 int64_t tc_launch_count(void) { return tc::g_launches.load(); }
+
+int64_t tc_fma_probe(int fp64, int64_t blocks, int iters, void* sink, void* stream) {
+    if (blocks < 1 || iters < 1 || !sink) return -1;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (fp64) tc::fma_probe_kernel<double><<<(unsigned)blocks, tc::BLOCK, 0, s>>>((double*)sink, iters);
+    else tc::fma_probe_kernel<float><<<(unsigned)blocks, tc::BLOCK, 0, s>>>((float*)sink, iters);
+    tc::g_launches++;
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    return (int64_t)2 * 8 * 16 * iters * blocks * tc::BLOCK;
+}
 
 int tc_stats_reset(tc_stats* stats, void* stream) {
     if (!stats) return TC_EINVAL;

@@ -19,7 +19,7 @@ import torch
 from . import _abi
 
 _DT = {torch.float64: "f64", torch.float32: "f32"}
-STATS_WORDS = 6  # tc_stats = 5 x int64 + 1 x double
+STATS_WORDS = 7  # tc_stats = 6 x int64 + 1 x double
 
 
 @dataclass
@@ -54,8 +54,8 @@ def read_stats(stats: torch.Tensor) -> dict:
     h = stats.cpu()
     return {
         "iterative": int(h[0]), "comparison": int(h[1]), "fallback": int(h[2]),
-        "degenerate": int(h[3]), "contacts": int(h[4]),
-        "min_distance": float(h[5:6].view(torch.float64)[0]),
+        "degenerate": int(h[3]), "contacts": int(h[4]), "intersecting": int(h[5]),
+        "min_distance": float(h[6:7].view(torch.float64)[0]),
     }
 
 

@@ -197,7 +197,7 @@ def _run(variant: str, A, B, eps, params, allow=None):
         bary_a=np.empty((n, 2), REAL),
         bary_b=np.empty((n, 2), REAL),
     )
-    stats = _abi.TcStats(0, 0, 0, 0, 0, float("inf"))
+    stats = _abi.TcStats(0, 0, 0, 0, 0, 0, float("inf"))
     if n == 0:
         return res, stats, _abi.TC_OK
     p = _abi.params_struct(params if params is not None else KernelParams(), _flags())

@@ -1,8 +1,18 @@
-"""Tolerance comparison of the fast (FMA-contracted) kernels against the oracle.
+"""Tie-aware tolerance comparison of the fast (FMA-contracted) kernels.
 
-North-star tolerance: |x - x_ref| <= tau * max(|x_ref|, L) with
-tau = 1e-9 (fp64) / 1e-4 (fp32) and L the pair's longest edge; discrete
-outputs (kind, fallback path, feature id) must match except at ties.
+North-star tolerance: |x - x_ref| <= tau * max(|x_ref|, L),
+tau = 1e-9 (fp64) / 1e-4 (fp32), L = the pair's longest edge.  Discrete
+outputs (kind, fallback path, feature / region / crossing ids) must equal
+the oracle's except where the oracle's own deciding margin
+(oracle.margins, tco_margins_* in oracle/tc_oracle_impl.h) is within the
+tolerance -- a tie.  An excused mismatch must still match the values of the
+alternative the GPU took (e.g. a pair that settled on the GPU but not in the
+oracle is compared with the oracle's iterative result).
+
+Contact points of ill-conditioned pairs (flat valleys: near-parallel or
+overlapping coplanar faces, where the minimiser is not unique) are exempt
+from the point check when a 1-ulp perturbation of the input moves the
+oracle's own points by more than tau/10; their distances are still checked.
 """
 
 from __future__ import annotations
@@ -10,13 +20,14 @@ from __future__ import annotations
 import numpy as np
 
 TAU = {np.dtype(np.float64): 1e-9, np.dtype(np.float32): 1e-4}
+VALUE_COLS = ("distance", "point_a", "point_b", "bary_a", "bary_b")
 
 
 def longest_edge(A, B):
     def sq(T):
         e = np.roll(T, -1, axis=1) - T
         return (e * e).sum(axis=2).max(axis=1)
-    return np.sqrt(np.maximum(sq(A.astype(np.float64)), sq(B.astype(np.float64))))
+    return np.sqrt(np.maximum(sq(np.asarray(A, np.float64)), sq(np.asarray(B, np.float64))))
 
 
 def rel_err(x, ref, L):
@@ -24,38 +35,125 @@ def rel_err(x, ref, L):
     ref = np.asarray(ref, np.float64)
     if x.ndim == 1:
         return np.abs(x - ref) / np.maximum(np.abs(ref), L)
-    return (np.abs(x - ref).max(axis=1)) / np.maximum(np.abs(ref).max(axis=1), L)
+    return np.abs(x - ref).max(axis=1) / np.maximum(np.abs(ref).max(axis=1), L)
 
 
-def compare_fast(O, variant, A, B, pkw, got, dtype, max_tie_frac=None):
-    """Compare one fast-mode result dict against the oracle; returns a report."""
+def _perturb(X, rng, dtype):
+    X = np.asarray(X, dtype)
+    steps = rng.integers(-1, 2, X.shape)
+    inf = np.array(np.inf, dtype)
+    up = np.nextafter(X, inf)
+    dn = np.nextafter(X, -inf)
+    return np.where(steps > 0, up, np.where(steps < 0, dn, X))
+
+
+def point_sensitivity(O, fn, A, B, dtype, base, reps=2, seed=1):
+    """Max relative point displacement of the oracle under 1-ulp input perturbations."""
+    rng = np.random.default_rng(seed)
+    L = longest_edge(A, B)
+    worst = np.zeros(len(A))
+    for _ in range(reps):
+        out = fn(_perturb(A, rng, dtype), _perturb(B, rng, dtype))
+        worst = np.maximum(worst, np.maximum(rel_err(out["point_a"], base["point_a"], L),
+                                             rel_err(out["point_b"], base["point_b"], L)))
+    return worst
+
+
+def compare_fast(O, variant, A, B, pkw, got, dtype, max_excused=None):
+    """Compare one fast-mode result (dict of numpy columns incl. ids) against the oracle."""
     dtype = np.dtype(dtype)
     tau = TAU[dtype]
+    A = np.ascontiguousarray(A, dtype)
+    B = np.ascontiguousarray(B, dtype)
+    n = len(A)
     p = O.make_params(**pkw)
-    eps = np.full(len(A), p.epsilon, dtype)
-    if variant == "comparison":
-        ref = O.comparison(A, B, eps, dtype)
-    elif variant == "iterative":
-        ref = O.iterative(A, B, p, eps, dtype)
-    else:
-        ref, _, _ = O.hybrid(A, B, p, eps, dtype=dtype)
+    eps = np.full(n, p.epsilon, dtype)
+    cm = O.comparison(A, B, eps, dtype)
+    it = O.iterative(A, B, p, eps, dtype)
+    mg = O.margins(A, B, p, eps, dtype)
     L = longest_edge(A, B)
-    path_ref = ref["ids"][:, 3] & 4
-    path_got = got["ids"][:, 3] & 4 if "ids" in got else path_ref
-    same = (ref["kind"] == got["kind"]) & (path_ref == path_got)
+    L2 = L * L
+    t_feat = mg[:, 0] <= tau * L2
+    t_kind_cmp = np.abs(mg[:, 1]) <= tau * L
+    t_cross = (mg[:, 2] <= tau * L) | (mg[:, 3] <= tau)
+    t_region = mg[:, 7] <= tau
+    t_settle = (np.abs(mg[:, 4]) <= tau * L2) | (np.abs(mg[:, 5]) <= tau * L)
+    t_contact = np.abs(mg[:, 6]) <= tau * L2
+
+    gid = got["ids"]
+    fb_got = (gid[:, 3] & 4) > 0
     if variant == "comparison":
-        same &= ref["ids"][:, 0] == got["ids"][:, 0] if "ids" in got else True
+        fb_got[:] = True
+        fb_ref = np.ones(n, bool)
+    elif variant == "iterative":
+        fb_got[:] = False
+        fb_ref = np.zeros(n, bool)
+    else:
+        fb_ref = (it["kind"] == 2)
+    path_ok = (fb_got == fb_ref) | t_settle
+    # the oracle result of the path the GPU took
+    ref = {k: np.where(fb_got.reshape((-1,) + (1,) * (cm[k].ndim - 1)), cm[k], it[k]) for k in cm}
+
+    # discrete checks on the GPU's path
+    cmp_rows = fb_got
+    it_rows = ~fb_got
+    kind_ok = (got["kind"] == ref["kind"])
+    kind_ok |= cmp_rows & (t_kind_cmp | t_cross)
+    kind_ok |= it_rows & (t_settle | t_contact)
+    feat_ok = np.ones(n, bool)
+    feat_ok[cmp_rows] = ((gid[cmp_rows, 0] == ref["ids"][cmp_rows, 0]) | t_feat[cmp_rows] | t_cross[cmp_rows])
+    region_ok = np.ones(n, bool)
+    region_ok[cmp_rows] = ((gid[cmp_rows, 1] == ref["ids"][cmp_rows, 1]) | ~feat_ok[cmp_rows]
+                           | (gid[cmp_rows, 0] != ref["ids"][cmp_rows, 0]) | t_region[cmp_rows])
+    cross_ok = np.ones(n, bool)
+    cross_ok[cmp_rows] = ((gid[cmp_rows, 2] == ref["ids"][cmp_rows, 2]) | t_cross[cmp_rows])
+
     d_err = rel_err(got["distance"], ref["distance"], L)
+    # a crossing-test tie switches the comparison answer between 0 and the
+    # best feature distance: either is the excused alternative
+    alt = cmp_rows & t_cross
+    d_err[alt] = np.minimum(d_err[alt], np.minimum(rel_err(got["distance"][alt], mg[alt, 8], L[alt]),
+                                                   rel_err(got["distance"][alt], np.zeros(int(alt.sum())), L[alt])))
     p_err = np.maximum(rel_err(got["point_a"], ref["point_a"], L), rel_err(got["point_b"], ref["point_b"], L))
-    mism = int((~same).sum())
-    if max_tie_frac is None:
-        max_tie_frac = 1e-3 if dtype == np.float64 else 2e-2
+    same_feature = it_rows | (gid[:, 0] == ref["ids"][:, 0]) & (gid[:, 2] == ref["ids"][:, 2])
+    pts_checked = same_feature & (p_err > tau)
+    ill = np.zeros(n, bool)
+    if pts_checked.any():
+        idx = np.nonzero(pts_checked)[0]
+        sens = np.zeros(len(idx))
+        sub_fb = fb_got[idx]
+        if (~sub_fb).any():
+            j = idx[~sub_fb]
+            base = {k: it[k][j] for k in it}
+            sens[~sub_fb] = point_sensitivity(O, lambda a, b: O.iterative(a, b, p, eps[j], dtype), A[j], B[j],
+                                              dtype, base)
+        if sub_fb.any():
+            j = idx[sub_fb]
+            base = {k: cm[k][j] for k in cm}
+            sens[sub_fb] = point_sensitivity(O, lambda a, b: O.comparison(a, b, eps[j], dtype), A[j], B[j],
+                                             dtype, base)
+        ill[idx] = sens > tau / 10
+    pts_bad = pts_checked & ~ill
+
+    # excused discrete mismatches (feature-id ties are reported separately:
+    # exactly tied features -- a vertex-face and the edge-edge tests through
+    # that vertex -- are common and harmless)
+    excused = (~(got["kind"] == ref["kind"]) | (fb_got != fb_ref) | ill
+               | (cmp_rows & (gid[:, 2] != ref["ids"][:, 2])))
+    feature_ties = cmp_rows & (gid[:, 0] != ref["ids"][:, 0])
+    if max_excused is None:
+        max_excused = 2e-3 if dtype == np.float64 else 3e-2
     rep = {
-        "variant": variant, "n": len(A), "discrete_mismatches": mism,
-        "distance_max_rel": float(d_err[same].max()) if same.any() else 0.0,
-        "point_max_rel": float(p_err[same].max()) if same.any() else 0.0,
-        "point_over_tol": int((p_err[same] > tau).sum()),
+        "variant": variant, "n": n,
+        "path_fail": int((~path_ok).sum()), "kind_fail": int((~kind_ok).sum()),
+        "feature_fail": int((~feat_ok).sum()), "region_fail": int((~region_ok).sum()),
+        "cross_fail": int((~cross_ok).sum()),
+        "distance_fail": int((d_err > tau).sum()), "distance_max_rel": float(d_err.max()) if n else 0.0,
+        "point_fail": int(pts_bad.sum()),
+        "excused": int(excused.sum()), "ill_conditioned_points": int(ill.sum()),
+        "feature_ties": int(feature_ties.sum()),
     }
-    rep["ok"] = (rep["distance_max_rel"] <= tau and mism <= max_tie_frac * len(A)
-                 and rep["point_over_tol"] <= max_tie_frac * len(A))
+    rep["ok"] = (rep["path_fail"] == 0 and rep["kind_fail"] == 0 and rep["feature_fail"] == 0
+                 and rep["region_fail"] == 0 and rep["cross_fail"] == 0 and rep["distance_fail"] == 0
+                 and rep["point_fail"] == 0 and rep["excused"] <= max_excused * max(n, 1))
     return rep
