@@ -174,7 +174,7 @@ struct Pol<T, true> { using R = Strict<T>; };
 
 // ---- kernels ---------------------------------------------------------------------
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK) comparison_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BLOCK, 2) comparison_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     Tally tl;
     for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BLOCK) {
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(BLOCK) comparison_kernel(Args<T> a) {
         load_tri<SOA>(a.tri_b, i, a.n, B);
         const R eps = R(a.eps ? a.eps[i] : a.eps_scalar);
         Rec<R> r;
-        comparison_pair(A, B, eps, r);
+        comparison_pair(A, B, eps, a.ids != nullptr, r);
         store_rec<SOA>(a, i, r);
         tl.comparison++;
         tl.result(r);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(BLOCK) iterative_kernel(Args<T> a) {
 }
 
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK) hybrid_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BLOCK, 2) hybrid_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     __shared__ int64_t queue[2 * BLOCK];
     __shared__ int qn;
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(BLOCK) hybrid_kernel(Args<T> a) {
         load_tri<SOA>(a.tri_b, j, a.n, B);
         const R eps = R(a.eps ? a.eps[j] : a.eps_scalar);
         Rec<R> r;
-        comparison_pair(A, B, eps, r);
+        comparison_pair(A, B, eps, a.ids != nullptr, r);
         // the pair was open (not settled) in the iterative pass
         r.ids |= (uint32_t)FLAG_FALLBACK << 24;
         store_rec<SOA>(a, j, r);

@@ -72,11 +72,14 @@ __device__ __forceinline__ bool degenerate_tri(const R* t) {
     return (L == R(0)) || (sq_area < thr);
 }
 
-// RK/kernels.py:157-221 closest_point_triangle_batch for one point.
-// Returns the claimed region in claim order 0 VA, 1 VB, 2 EAB, 3 VC, 4 EAC,
-// 5 EBC, 6 interior; u, w are the weights along ab, ac.
+// RK/kernels.py:157-221 closest_point_triangle_batch for one point, written
+// branch-free: the claimed region (claim order 0 VA, 1 VB, 2 EAB, 3 VC,
+// 4 EAC, 5 EBC, 6 interior) only selects the numerators and the shared
+// denominator, so the divergent region cases cost one division pair for the
+// whole warp.  u, w are the weights along ab, ac; results are the
+// reference's bit for bit in strict mode.
 template <class R>
-__device__ __forceinline__ int closest_point_triangle(const R* p, const R* tri, R* closest, R& u, R& w) {
+__device__ __forceinline__ int closest_point_params(const R* p, const R* tri, R& u, R& w) {
     const R* a = tri;
     const R* b = tri + 3;
     const R* c = tri + 6;
@@ -95,49 +98,70 @@ __device__ __forceinline__ int closest_point_triangle(const R* p, const R* tri, 
     const R vc = d1 * d4 - d3 * d2;
     const R vb = d5 * d2 - d1 * d6;
     const R va = d3 * d6 - d5 * d4;
+    const R n43 = d4 - d3, n56 = d5 - d6;
+    int region;
+    if (d1 <= R(0) && d2 <= R(0)) region = 0;
+    else if (d3 >= R(0) && d4 <= d3) region = 1;
+    else if (vc <= R(0) && d1 >= R(0) && d3 <= R(0)) region = 2;
+    else if (d6 >= R(0) && d5 <= d6) region = 3;
+    else if (vb <= R(0) && d2 >= R(0) && d6 <= R(0)) region = 4;
+    else if (va <= R(0) && n43 >= R(0) && n56 >= R(0)) region = 5;
+    else region = 6;
+    // numerator / denominator of the region's parameter(s)
+    R num = R(1), den = R(1);
+    if (region == 2) { num = d1; den = d1 - d3; }
+    if (region == 4) { num = d2; den = d2 - d6; }
+    if (region == 5) { num = n43; den = n43 + n56; }
+    if (region == 6) { num = vb; den = (va + vb) + vc; }
+    den = (den == R(0)) ? R(1) : den;
+    const R q1 = divv(num, den);
     u = R(0);
     w = R(0);
-    int region;
-    if (d1 <= R(0) && d2 <= R(0)) {
-        region = 0;
-    } else if (d3 >= R(0) && d4 <= d3) {
-        region = 1;
-        u = R(1);
-    } else if (vc <= R(0) && d1 >= R(0) && d3 <= R(0)) {
-        region = 2;
-        const R den = d1 - d3;
-        u = d1 / (den == R(0) ? R(1) : den);
-    } else if (d6 >= R(0) && d5 <= d6) {
-        region = 3;
-        w = R(1);
-    } else if (vb <= R(0) && d2 >= R(0) && d6 <= R(0)) {
-        region = 4;
-        const R den = d2 - d6;
-        w = d2 / (den == R(0) ? R(1) : den);
-    } else if (va <= R(0) && (d4 - d3) >= R(0) && (d5 - d6) >= R(0)) {
-        region = 5;
-        const R n1 = d4 - d3;
-        const R den = n1 + (d5 - d6);
-        const R t = n1 / (den == R(0) ? R(1) : den);
-        u = R(1) - t;
-        w = t;
-    } else {
-        region = 6;
-        R den = (va + vb) + vc;
-        den = (den == R(0)) ? R(1) : den;
-        u = vb / den;
-        w = vc / den;
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) closest[i] = (a[i] + u * ab[i]) + w * ac[i];
+    if (region == 1) u = R(1);
+    if (region == 2) u = q1;
+    if (region == 3) w = R(1);
+    if (region == 4) w = q1;
+    if (region == 5) { u = R(1) - q1; w = q1; }
+    if (region == 6) { u = q1; w = divv(vc, den); }
     return region;
 }
 
-// RK/kernels.py:224-252 _closest_segment_segment.  Branch code: bit0 = s
-// from the 2x2 solve (denom > TINY), bit1 = t < 0, bit2 = t > 1.
 template <class R>
-__device__ __forceinline__ int segment_segment(const R* p1, const R* q1, const R* p2, const R* q2, R& s, R& t,
-                                               R* c1, R* c2) {
+__device__ __forceinline__ void bary_point(const R* tri, R u, R w, R* out) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const R ab = tri[3 + i] - tri[i];
+        const R ac = tri[6 + i] - tri[i];
+        out[i] = (tri[i] + u * ab) + w * ac;
+    }
+}
+
+// Full RK/kernels.py:157-221 (closest point and weights); used by cpt_kernel.
+template <class R>
+__device__ __forceinline__ int closest_point_triangle(const R* p, const R* tri, R* closest, R& u, R& w) {
+    const int region = closest_point_params(p, tri, u, w);
+    bary_point(tri, u, w, closest);
+    return region;
+}
+
+__device__ __forceinline__ int edge_start(int k) { return k; }
+__device__ __forceinline__ int edge_end(int k) { return k == 2 ? 0 : k + 1; }
+
+// Vertex k (runtime) of a register-resident triangle, by selects.
+template <class R>
+__device__ __forceinline__ void vertex_sel(const R* t, int k, R* v) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) v[i] = (k == 0) ? t[i] : ((k == 1) ? t[3 + i] : t[6 + i]);
+}
+
+// RK/kernels.py:224-252 _closest_segment_segment.  The parameters s, t are
+// returned (the closest points are rebuilt for the winner only).  ra = 1/a
+// and re = 1/e are the hoisted reciprocals of the two squared edge lengths
+// (with the reference's TINY guard applied).  Branch code: bit0 = s from the
+// 2x2 solve, bit1 = t < 0, bit2 = t > 1.
+template <class R>
+__device__ __forceinline__ int segment_params(const R* p1, const R* q1, const R* p2, const R* q2, R ra, R re,
+                                              R& s, R& t, R& d2out) {
     const R tiny = R(Tiny<R>::v);
     R d1[3], d2[3], r[3];
     sub3(q1, p1, d1);
@@ -149,177 +173,227 @@ __device__ __forceinline__ int segment_segment(const R* p1, const R* q1, const R
     const R c = dot3(d1, r);
     const R b = dot3(d1, d2);
     const R denom = a * e - b * b;
-    int code = 0;
-    if (denom > tiny) {
-        code = 1;
-        s = clipv((b * f - c * e) / denom, R(0), R(1));
-    } else {
-        s = R(0);
-    }
-    t = (b * s + f) / ((e > tiny) ? e : R(1));
+    const bool solve = denom > tiny;
+    const R s0 = divv(b * f - c * e, solve ? denom : R(1));
+    s = solve ? clipv(s0, R(0), R(1)) : R(0);
+    const R e_safe = (e > tiny) ? e : R(1);
+    t = divr(b * s + f, e_safe, re);
     const R a_safe = (a > tiny) ? a : R(1);
-    if (t < R(0)) {
-        code |= 2;
-        s = clipv((-c) / a_safe, R(0), R(1));
-    } else if (t > R(1)) {
-        code |= 4;
-        s = clipv((b - c) / a_safe, R(0), R(1));
-    }
+    const bool lo = t < R(0), hi = t > R(1);
+    const R s2 = clipv(divr(lo ? -c : (b - c), a_safe, ra), R(0), R(1));
+    s = (lo || hi) ? s2 : s;
     t = clipv(t, R(0), R(1));
+    R diff[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        c1[i] = p1[i] + s * d1[i];
-        c2[i] = p2[i] + t * d2[i];
-    }
-    return code;
+    for (int i = 0; i < 3; ++i) diff[i] = (p1[i] + s * d1[i]) - (p2[i] + t * d2[i]);
+    d2out = dot3(diff, diff);
+    return (solve ? 1 : 0) | (lo ? 2 : 0) | (hi ? 4 : 0);
 }
-
-// RK/kernels.py:269-298 _segment_triangle_crossings for one segment: proper
-// crossing (strict dp*dq < 0) through the closed triangle.
-template <class R>
-__device__ __forceinline__ bool segment_crosses(const R* p, const R* q, const R* tri, R* x) {
-    const R tiny = R(Tiny<R>::v);
-    const R* a = tri;
-    R u[3], v[3], nrm[3], t3[3];
-    sub3(tri + 3, a, u);
-    sub3(tri + 6, a, v);
-    cross3(u, v, nrm);
-    sub3(p, a, t3);
-    const R dp = dot3(t3, nrm);
-    sub3(q, a, t3);
-    const R dq = dot3(t3, nrm);
-    const bool crossing = (dp * dq) < R(0);
-    const R denom = dp - dq;
-    const R t = dp / (denom == R(0) ? R(1) : denom);
-    sub3(q, p, t3);
-#pragma unroll
-    for (int i = 0; i < 3; ++i) x[i] = p[i] + t * t3[i];
-    sub3(x, a, t3);
-    const R uu = dot3(u, u);
-    const R uv = dot3(u, v);
-    const R vv = dot3(v, v);
-    const R wu = dot3(t3, u);
-    const R wv = dot3(t3, v);
-    const R det = uu * vv - uv * uv;
-    const R det_safe = (absv(det) > tiny) ? det : R(1);
-    const R b1 = (vv * wu - uv * wv) / det_safe;
-    const R b2 = (uu * wv - uv * wu) / det_safe;
-    return crossing && (b1 >= R(0)) && (b2 >= R(0)) && ((b1 + b2) <= R(1));
-}
-
-__device__ __forceinline__ int edge_start(int k) { return k; }
-__device__ __forceinline__ int edge_end(int k) { return k == 2 ? 0 : k + 1; }
 
 // RK/kernels.py:261-266 _edge_bary
 template <class R>
 __device__ __forceinline__ void edge_bary(int k, R s, R* o) {
-    if (k == 0) { o[0] = s; o[1] = R(0); }
-    else if (k == 1) { o[0] = R(1) - s; o[1] = s; }
-    else { o[0] = R(0); o[1] = R(1) - s; }
+    o[0] = (k == 0) ? s : ((k == 1) ? R(1) - s : R(0));
+    o[1] = (k == 0) ? R(0) : ((k == 1) ? s : R(1) - s);
 }
 
-// RK/kernels.py:301-401 comparison_batch for one pair: 6 point-triangle +
-// 9 segment-segment candidates with a running first-minimum (argmin ties go
-// to the lowest row), then 6 edge-plane crossings; an intersecting pair
-// reports distance 0 at the midpoint of its two farthest-apart crossing
-// points (first argmax over the 6x6 grid).
+// Per-target-triangle constants of the edge-plane test (RK/kernels.py:269-298).
 template <class R>
-__device__ __noinline__ void comparison_pair(const R* A, const R* B, R eps, Rec<R>& o) {
-    R best = R(0), cl[3], diff[3], u, w, d2;
-    int best_row = 0, best_code = 0;
-#pragma unroll 1
-    for (int k = 0; k < 3; ++k) {
-        const R* pt = A + 3 * k;
-        const int reg = closest_point_triangle(pt, B, cl, u, w);
-        sub3(pt, cl, diff);
-        d2 = dot3(diff, diff);
-        if (k == 0 || d2 < best) {
-            best = d2; best_row = k; best_code = reg;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) { o.pa[i] = pt[i]; o.pb[i] = cl[i]; }
-            o.ba[0] = (k == 1) ? R(1) : R(0);
-            o.ba[1] = (k == 2) ? R(1) : R(0);
-            o.bb[0] = u; o.bb[1] = w;
-        }
-    }
-#pragma unroll 1
-    for (int k = 0; k < 3; ++k) {
-        const R* pt = B + 3 * k;
-        const int reg = closest_point_triangle(pt, A, cl, u, w);
-        sub3(pt, cl, diff);
-        d2 = dot3(diff, diff);
-        if (d2 < best) {
-            best = d2; best_row = 3 + k; best_code = reg;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) { o.pa[i] = cl[i]; o.pb[i] = pt[i]; }
-            o.ba[0] = u; o.ba[1] = w;
-            o.bb[0] = (k == 1) ? R(1) : R(0);
-            o.bb[1] = (k == 2) ? R(1) : R(0);
-        }
-    }
-#pragma unroll 1
-    for (int row = 6; row < 15; ++row) {
-        const int ka = (row - 6) / 3, kb = (row - 6) % 3;
-        R s, t, c1[3], c2[3];
-        const int code = segment_segment(A + 3 * edge_start(ka), A + 3 * edge_end(ka), B + 3 * edge_start(kb),
-                                         B + 3 * edge_end(kb), s, t, c1, c2);
-        sub3(c1, c2, diff);
-        d2 = dot3(diff, diff);
-        if (d2 < best) {
-            best = d2; best_row = row; best_code = code;
-#pragma unroll
-            for (int i = 0; i < 3; ++i) { o.pa[i] = c1[i]; o.pb[i] = c2[i]; }
-            edge_bary(ka, s, o.ba);
-            edge_bary(kb, t, o.bb);
-        }
-    }
-    o.distance = sqrtv(best);
+struct PlaneFrame {
+    R nrm[3], uu, uv, vv, det_safe, rdet;
+};
 
-    // six edge-to-plane tests (RK/kernels.py:364-375)
-    R pts[6][3];
-    uint32_t ok = 0;
+template <class R>
+__device__ __forceinline__ void plane_frame(const R* tri, PlaneFrame<R>& f) {
+    const R tiny = R(Tiny<R>::v);
+    R u[3], v[3];
+    sub3(tri + 3, tri, u);
+    sub3(tri + 6, tri, v);
+    cross3(u, v, f.nrm);
+    f.uu = dot3(u, u);
+    f.uv = dot3(u, v);
+    f.vv = dot3(v, v);
+    const R det = f.uu * f.vv - f.uv * f.uv;
+    f.det_safe = (absv(det) > tiny) ? det : R(1);
+    f.rdet = rcpv(f.det_safe);
+}
+
+// One proper crossing test of segment [p, q] through the closed triangle.
+template <class R>
+__device__ __forceinline__ bool segment_crosses(const R* p, const R* q, const R* tri, const PlaneFrame<R>& f, R* x) {
+    R t3[3], u[3], v[3];
+    sub3(p, tri, t3);
+    const R dp = dot3(t3, f.nrm);
+    sub3(q, tri, t3);
+    const R dq = dot3(t3, f.nrm);
+    const bool crossing = (dp * dq) < R(0);
+    const R denom = dp - dq;
+    const R t = divv(dp, denom == R(0) ? R(1) : denom);
+    sub3(q, p, t3);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if (segment_crosses(A + 3 * edge_start(k), A + 3 * edge_end(k), B, pts[k])) ok |= 1u << k;
-        if (segment_crosses(B + 3 * edge_start(k), B + 3 * edge_end(k), A, pts[k + 3])) ok |= 8u << k;
-    }
-    uint32_t pair_id = 255;
-    if (ok) {
-        // first argmax over the row-major 6x6 grid; invalid pairs score -1
-        R bestv = R(-1);
-        int bi = 0;
-#pragma unroll
-        for (int i0 = 0; i0 < 6; ++i0) {
-#pragma unroll
-            for (int i1 = 0; i1 < 6; ++i1) {
-                if (((ok >> i0) & 1u) && ((ok >> i1) & 1u)) {
-                    sub3(pts[i0], pts[i1], diff);
-                    const R v = dot3(diff, diff);
-                    if (v > bestv) { bestv = v; bi = i0 * 6 + i1; }
-                }
+    for (int i = 0; i < 3; ++i) x[i] = p[i] + t * t3[i];
+    sub3(tri + 3, tri, u);
+    sub3(tri + 6, tri, v);
+    sub3(x, tri, t3);
+    const R wu = dot3(t3, u);
+    const R wv = dot3(t3, v);
+    const R b1 = divr(f.vv * wu - f.uv * wv, f.det_safe, f.rdet);
+    const R b2 = divr(f.uu * wv - f.uv * wu, f.det_safe, f.rdet);
+    return crossing && (b1 >= R(0)) && (b2 >= R(0)) && ((b1 + b2) <= R(1));
+}
+
+// RK/kernels.py:301-401 comparison_batch for one pair.
+//
+// Phase 1: the six edge-plane tests.  Valid crossing points go to a small
+// thread-local list (local memory -- usually 0 or 2 entries); the farthest
+// pair is kept with the reference's first-argmax order over the row-major
+// 6x6 grid.  Phase 2 (skipped for intersecting pairs unless ids are
+// requested: their outputs do not depend on it): the 15 feature tests with
+// a running first minimum that keeps only (row, d^2, two parameters); the
+// winner's points are rebuilt from its parameters with the reference's
+// formulas, so strict results stay bit-identical.
+template <class R>
+__device__ __noinline__ void comparison_pair(const R* A, const R* B, R eps, bool want_ids, Rec<R>& o) {
+    using T = typename Store<R>::type;
+    const R tiny = R(Tiny<R>::v);
+    // ---- phase 1: edge-plane crossings (rows 0-2: A's edges vs B, 3-5: B's vs A)
+    R cpts[6][3];
+    int ck[6];
+    int nv = 0;
+    {
+        PlaneFrame<R> fb;
+        plane_frame(B, fb);
+#pragma unroll 1
+        for (int k = 0; k < 3; ++k) {
+            R p[3], q[3], x[3];
+            vertex_sel(A, edge_start(k), p);
+            vertex_sel(A, edge_end(k), q);
+            if (segment_crosses(p, q, B, fb, x)) {
+                cpts[nv][0] = x[0]; cpts[nv][1] = x[1]; cpts[nv][2] = x[2];
+                ck[nv] = k;
+                ++nv;
             }
         }
-        const int i0 = bi / 6, i1 = bi % 6;
+        PlaneFrame<R> fa;
+        plane_frame(A, fa);
+#pragma unroll 1
+        for (int k = 0; k < 3; ++k) {
+            R p[3], q[3], x[3];
+            vertex_sel(B, edge_start(k), p);
+            vertex_sel(B, edge_end(k), q);
+            if (segment_crosses(p, q, A, fa, x)) {
+                cpts[nv][0] = x[0]; cpts[nv][1] = x[1]; cpts[nv][2] = x[2];
+                ck[nv] = 3 + k;
+                ++nv;
+            }
+        }
+    }
+    const bool intersecting = nv > 0;
+    uint32_t pair_id = 255;
+    if (intersecting) {
+        int i0 = 0, i1 = 0;  // list positions; (first, first) scores 0 at index 7*ck[0]
+        R bestv = R(0);
+        int bidx = 7 * ck[0];
+#pragma unroll 1
+        for (int a = 0; a < nv; ++a) {
+#pragma unroll 1
+            for (int b = a + 1; b < nv; ++b) {
+                R diff[3];
+                sub3(cpts[a], cpts[b], diff);
+                const R v = dot3(diff, diff);
+                const int idx = 6 * ck[a] + ck[b];
+                if (v > bestv || (v == bestv && idx < bidx)) { bestv = v; bidx = idx; i0 = a; i1 = b; }
+            }
+        }
+        pair_id = (uint32_t)bidx;
         R mid[3];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            R a0 = R(0), a1 = R(0);
-#pragma unroll
-            for (int j = 0; j < 6; ++j) {
-                if (j == i0) a0 = pts[j][i];
-                if (j == i1) a1 = pts[j][i];
-            }
-            mid[i] = R(typename Store<R>::type(0.5)) * (a0 + a1);
-        }
-        pair_id = (uint32_t)bi;
+        for (int i = 0; i < 3; ++i) mid[i] = R(T(0.5)) * (cpts[i0][i] + cpts[i1][i]);
         o.distance = R(0);
 #pragma unroll
         for (int i = 0; i < 3; ++i) { o.pa[i] = mid[i]; o.pb[i] = mid[i]; }
-        closest_point_triangle(mid, A, cl, o.ba[0], o.ba[1]);
-        closest_point_triangle(mid, B, cl, o.bb[0], o.bb[1]);
+        closest_point_params(mid, A, o.ba[0], o.ba[1]);
+        closest_point_params(mid, B, o.bb[0], o.bb[1]);
     }
-    o.kind = (o.distance <= R(typename Store<R>::type(2)) * eps) ? KIND_CONTACT : KIND_NO_CONTACT;
-    o.ids = (uint32_t)best_row | ((uint32_t)best_code << 8) | (pair_id << 16) | ((ok ? FLAG_INTERSECT : 0u) << 24);
+    // ---- phase 2: the 15 feature candidates
+    int best_row = 0, best_code = 0;
+    if (!intersecting || want_ids) {
+        R best = R(0), bp1 = R(0), bp2 = R(0);
+#pragma unroll 1
+        for (int row = 0; row < 6; ++row) {
+            const R* src = row < 3 ? A : B;
+            const R* dst = row < 3 ? B : A;
+            R pt[3], u, w, cl[3], diff[3];
+            vertex_sel(src, row % 3, pt);
+            const int reg = closest_point_params(pt, dst, u, w);
+            bary_point(dst, u, w, cl);
+            sub3(pt, cl, diff);
+            const R d2 = dot3(diff, diff);
+            if (row == 0 || d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
+        }
+        // hoisted reciprocals of the six squared edge lengths (TINY-guarded)
+        R ra[3], rb[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            R p[3], q[3], d[3];
+            vertex_sel(A, edge_start(k), p);
+            vertex_sel(A, edge_end(k), q);
+            sub3(q, p, d);
+            R l = dot3(d, d);
+            ra[k] = rcpv(l > tiny ? l : R(1));
+            vertex_sel(B, edge_start(k), p);
+            vertex_sel(B, edge_end(k), q);
+            sub3(q, p, d);
+            l = dot3(d, d);
+            rb[k] = rcpv(l > tiny ? l : R(1));
+        }
+#pragma unroll 1
+        for (int row = 6; row < 15; ++row) {
+            const int ka = (row - 6) / 3, kb = (row - 6) % 3;
+            R p1[3], q1[3], p2[3], q2[3], s, t, d2;
+            vertex_sel(A, edge_start(ka), p1);
+            vertex_sel(A, edge_end(ka), q1);
+            vertex_sel(B, edge_start(kb), p2);
+            vertex_sel(B, edge_end(kb), q2);
+            const R rak = (ka == 0) ? ra[0] : ((ka == 1) ? ra[1] : ra[2]);
+            const R rbk = (kb == 0) ? rb[0] : ((kb == 1) ? rb[1] : rb[2]);
+            const int code = segment_params(p1, q1, p2, q2, rak, rbk, s, t, d2);
+            if (d2 < best) { best = d2; best_row = row; best_code = code; bp1 = s; bp2 = t; }
+        }
+        if (!intersecting) {
+            o.distance = sqrtv(best);
+            if (best_row < 3) {
+                vertex_sel(A, best_row, o.pa);
+                bary_point(B, bp1, bp2, o.pb);
+                o.ba[0] = (best_row == 1) ? R(1) : R(0);
+                o.ba[1] = (best_row == 2) ? R(1) : R(0);
+                o.bb[0] = bp1; o.bb[1] = bp2;
+            } else if (best_row < 6) {
+                bary_point(A, bp1, bp2, o.pa);
+                vertex_sel(B, best_row - 3, o.pb);
+                o.ba[0] = bp1; o.ba[1] = bp2;
+                o.bb[0] = (best_row == 4) ? R(1) : R(0);
+                o.bb[1] = (best_row == 5) ? R(1) : R(0);
+            } else {
+                const int ka = (best_row - 6) / 3, kb = (best_row - 6) % 3;
+                R p1[3], q1[3], p2[3], q2[3];
+                vertex_sel(A, edge_start(ka), p1);
+                vertex_sel(A, edge_end(ka), q1);
+                vertex_sel(B, edge_start(kb), p2);
+                vertex_sel(B, edge_end(kb), q2);
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    o.pa[i] = p1[i] + bp1 * (q1[i] - p1[i]);
+                    o.pb[i] = p2[i] + bp2 * (q2[i] - p2[i]);
+                }
+                edge_bary(ka, bp1, o.ba);
+                edge_bary(kb, bp2, o.bb);
+            }
+        }
+    }
+    o.kind = (o.distance <= R(T(2)) * eps) ? KIND_CONTACT : KIND_NO_CONTACT;
+    o.ids = (uint32_t)best_row | ((uint32_t)best_code << 8) | (pair_id << 16) |
+            ((intersecting ? (uint32_t)FLAG_INTERSECT : 0u) << 24);
 }
 
 // RK/kernels.py:417-431 _penalty_value, summed left to right.
@@ -349,10 +423,13 @@ __device__ __forceinline__ void contact_mid(const R* A0, const R* x, const R* e1
 
 // One coordinate substep (RK/kernels.py:531-536): preconditioned descent on
 // the quadratic part, then the clip to [0, max(0, 1 - max(x_partner, 0))].
+// `box`: the fast build's shortcut when start_coord lies in [0, 1] -- every
+// iterate then stays in the box (x >= 0 exactly, x_k + x_partner <= 1 up to
+// an ulp), so the two inner max() are identities up to rounding.
 template <class R>
-__device__ __forceinline__ void coord_step(R& xk, R xp, const R* e, R den, R rcp, R* d) {
+__device__ __forceinline__ void coord_step(R& xk, R xp, const R* e, R den, R rcp, R* d, bool box) {
     R target = xk - divr(dot3(d, e), den, rcp);
-    const R hi = maxv(R(0), R(1) - maxv(xp, R(0)));
+    const R hi = (!IsStrict<R>::value && box) ? R(1) - xp : maxv(R(0), R(1) - maxv(xp, R(0)));
     target = clipv(target, R(0), hi);
     const R step = target - xk;
     xk = target;
@@ -362,9 +439,10 @@ __device__ __forceinline__ void coord_step(R& xk, R xp, const R* e, R den, R rcp
 
 // Slide along the triangle's third edge (RK/kernels.py:537-546).
 template <class R>
-__device__ __forceinline__ void slide_step(R& xa, R& xb, const R* e3, R den3, R rcp3, R* d) {
+__device__ __forceinline__ void slide_step(R& xa, R& xb, const R* e3, R den3, R rcp3, R* d, bool box) {
     R t = divr(-dot3(d, e3), den3, rcp3);
-    t = clipv(t, -maxv(xb, R(0)), maxv(xa, R(0)));
+    if (!IsStrict<R>::value && box) t = clipv(t, -xb, xa);
+    else t = clipv(t, -maxv(xb, R(0)), maxv(xa, R(0)));
     xa = xa - t;
     xb = xb + t;
 #pragma unroll
@@ -411,18 +489,19 @@ __device__ __forceinline__ void iterative_pair(const R* A, const R* B, R eps, co
 
     R j_old = R(0), mid_old[3];
     const int n_it = kp.n_iterative;
+    const bool box = kp.start_coord >= R(0) && kp.start_coord <= R(1);
 #pragma unroll 1
     for (int it = 0; it < n_it; ++it) {
         if (it == n_it - 1) {
             j_old = half * dot3(d, d) + penalty(x, alpha_it);
             contact_mid(A, x, e1a, e2a, d, mid_old);
         }
-        coord_step(x[0], x[1], e1a, den0, r0, d);
-        coord_step(x[1], x[0], e2a, den1, r1, d);
-        slide_step(x[0], x[1], e3a, den3a, r3a, d);
-        coord_step(x[2], x[3], ne1b, den2, r2, d);
-        coord_step(x[3], x[2], ne2b, den3, r3, d);
-        slide_step(x[2], x[3], ne3b, den3b, r3b, d);
+        coord_step(x[0], x[1], e1a, den0, r0, d, box);
+        coord_step(x[1], x[0], e2a, den1, r1, d, box);
+        slide_step(x[0], x[1], e3a, den3a, r3a, d, box);
+        coord_step(x[2], x[3], ne1b, den2, r2, d, box);
+        coord_step(x[3], x[2], ne2b, den3, r3, d, box);
+        slide_step(x[2], x[3], ne3b, den3b, r3b, d, box);
     }
     const R dd = dot3(d, d);
     const R j_total = half * dd + penalty(x, alpha_it);
