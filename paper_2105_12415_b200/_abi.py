@@ -9,6 +9,7 @@ product entry points raise.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libtricontact_b200.so"
@@ -89,7 +90,7 @@ def load(path: Path | str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("TC_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise TricontactError(
             f"{p} is missing: build it with `python -m paper_2105_12415_b200._build` "

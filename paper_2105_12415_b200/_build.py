@@ -44,14 +44,17 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Compile the library (``out``/``defines``: experiment variants, e.g. launch bounds)."""
+    target = Path(out) if out else LIB
+    if out is None and not defines and not force and not stale():
         return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", str(tmp), *map(str, SOURCES)]
+    tmp = target.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
+           "-o", str(tmp), *map(str, SOURCES)]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -26,6 +26,13 @@
 namespace tc {
 
 constexpr int BLOCK = 256;
+// resident CTAs per SM the register allocator targets (launch bounds)
+#ifndef TC_ITER_MINB
+#define TC_ITER_MINB 2
+#endif
+#ifndef TC_HYBRID_MINB
+#define TC_HYBRID_MINB 2
+#endif
 
 static std::atomic<int64_t> g_launches{0};
 static thread_local char g_err[512] = "";
@@ -77,6 +84,41 @@ __device__ __forceinline__ void load_tri(const T* __restrict__ src, int64_t i, i
         const T* p = src + 9 * i;
 #pragma unroll
         for (int k = 0; k < 9; ++k) t[k] = R(__ldg(p + k));
+    }
+}
+
+// Base vertices (v0 of A and B) of pair i, re-read after the sweep loop.
+template <bool SOA, class R, typename T>
+__device__ __forceinline__ void load_base(const Args<T>& a, int64_t i, R* A0, R* B0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        A0[k] = R(__ldg(SOA ? a.tri_a + k * a.n + i : a.tri_a + 9 * i + k));
+        B0[k] = R(__ldg(SOA ? a.tri_b + k * a.n + i : a.tri_b + 9 * i + k));
+    }
+}
+
+// Iterative kernel for one pair: the reference's operation order in strict
+// mode, the Gram-matrix form in the fast build (tc_pair.cuh).
+template <bool SOA, class R, typename T>
+__device__ __forceinline__ void run_iterative(const Args<T>& a, int64_t i, const R* A, const R* B, R eps,
+                                              const KP<R>& kp, Rec<R>& r) {
+    if constexpr (IsStrict<R>::value) {
+        iterative_pair(A, B, eps, kp, r, [&](R* A0, R* B0) { load_base<SOA>(a, i, A0, B0); });
+    } else {
+        iterative_pair_gram(A, B, eps, kp, r, [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4) {
+            R At[9], Bt[9];
+            load_tri<SOA>(a.tri_a, i, a.n, At);
+            load_tri<SOA>(a.tri_b, i, a.n, Bt);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                A0[k] = At[k];
+                B0[k] = Bt[k];
+                E0[k] = At[3 + k] - At[k];
+                E1[k] = At[6 + k] - At[k];
+                E3[k] = Bt[k] - Bt[3 + k];
+                E4[k] = Bt[k] - Bt[6 + k];
+            }
+        });
     }
 }
 
@@ -173,37 +215,153 @@ template <typename T>
 struct Pol<T, true> { using R = Strict<T>; };
 
 // ---- kernels ---------------------------------------------------------------------
+
+// Block-shared work queues of pair indices for the compacted comparison
+// phases: q1 holds pairs awaiting phase 1 (crossings), q2 pairs awaiting
+// phase 2 (features).  Bit 62 of a q2 entry marks "ids only".
+struct Queues {
+    int64_t q1[2 * BLOCK];
+    int64_t q2[2 * BLOCK];
+    int n1, n2;
+};
+
+// Shared-memory crossing-point scratch of the calling thread (6 x 3 values).
+template <class R>
+__device__ __forceinline__ Scratch<R> thread_scratch() {
+    using T = typename Store<R>::type;
+    extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
+    Scratch<R> s;
+    s.p = reinterpret_cast<T*>(tc_dyn_smem) + threadIdx.x;
+    s.stride = BLOCK;
+    return s;
+}
+template <typename T>
+constexpr size_t scratch_bytes() { return sizeof(T) * 18 * BLOCK; }
+constexpr int64_t IDS_ONLY = int64_t(1) << 62;
+
+// Warp-aggregated append (all 32 lanes of the warp must call it).
+__device__ __forceinline__ void push(int64_t* q, int* n, bool pred, int64_t v) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(n, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (pred) q[base + __popc(m & ((1u << lane) - 1u))] = v;
+}
+
+template <bool SOA, class R, typename T>
+__device__ __forceinline__ void load_pair(const Args<T>& a, int64_t j, R* A, R* B, R& eps) {
+    load_tri<SOA>(a.tri_a, j, a.n, A);
+    load_tri<SOA>(a.tri_b, j, a.n, B);
+    eps = R(a.eps ? a.eps[j] : a.eps_scalar);
+}
+
+// Run whole batches (BLOCK pairs, or the remainder when `final_`) from the
+// queues until neither holds a full batch.  Block-uniform; every batch runs
+// on full warps.  `fallback_flag`: hybrid results carry FLAG_FALLBACK.
+template <bool SOA, class R, typename T>
+__device__ __forceinline__ void drain(const Args<T>& a, Queues& Q, Tally& tl, bool final_, uint32_t fallback_flag) {
+    const bool want_ids = a.ids != nullptr;
+    while (true) {
+        const int c1 = Q.n1, c2 = Q.n2;
+        __syncthreads();  // everyone has read the counts before they change
+        int which = 0;
+        if (c1 >= BLOCK || (final_ && c1 > 0)) which = 1;
+        else if (c2 >= BLOCK || (final_ && c2 > 0)) which = 2;
+        if (!which) break;
+        const int c = which == 1 ? c1 : c2;
+        const int m = c < BLOCK ? c : BLOCK;
+        int64_t e = -1;
+        if ((int)threadIdx.x < m) e = (which == 1 ? Q.q1 : Q.q2)[c - m + threadIdx.x];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (which == 1) Q.n1 = c - m;
+            else Q.n2 = c - m;
+        }
+        bool push2 = false;
+        int64_t e2 = 0;
+        if (e >= 0) {
+            const int64_t j = e & (IDS_ONLY - 1);
+            R A[9], B[9], eps;
+            load_pair<SOA>(a, j, A, B, eps);
+            Rec<R> r;
+            if (which == 1) {
+                tl.comparison++;
+                if (comparison_phase1(A, B, eps, thread_scratch<R>(), r)) {
+                    r.ids |= fallback_flag << 24;
+                    store_rec<SOA>(a, j, r);
+                    tl.result(r);
+                    push2 = want_ids;
+                    e2 = j | IDS_ONLY;
+                } else {
+                    push2 = true;
+                    e2 = j;
+                }
+            } else {
+                const bool ids_only = (e & IDS_ONLY) != 0;
+                comparison_phase2(A, B, eps, ids_only, r);
+                if (ids_only) {
+                    a.ids[4 * j] = (uint8_t)(r.ids & 0xFF);
+                    a.ids[4 * j + 1] = (uint8_t)((r.ids >> 8) & 0xFF);
+                } else {
+                    r.ids |= fallback_flag << 24;
+                    store_rec<SOA>(a, j, r);
+                    tl.result(r);
+                }
+            }
+        }
+        if (which == 1) push(Q.q2, &Q.n2, push2, e2);
+        __syncthreads();
+    }
+}
+
 template <typename T, bool STRICT, bool SOA>
 __global__ void __launch_bounds__(BLOCK, 2) comparison_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
+    __shared__ Queues Q;
     Tally tl;
-    for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BLOCK) {
-        R A[9], B[9];
-        load_tri<SOA>(a.tri_a, i, a.n, A);
-        load_tri<SOA>(a.tri_b, i, a.n, B);
-        const R eps = R(a.eps ? a.eps[i] : a.eps_scalar);
-        Rec<R> r;
-        comparison_pair(A, B, eps, a.ids != nullptr, r);
-        store_rec<SOA>(a, i, r);
-        tl.comparison++;
-        tl.result(r);
+    if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
+    __syncthreads();
+    const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t i = tile * BLOCK + threadIdx.x;
+        bool need2 = false;
+        int64_t e2 = 0;
+        if (i < a.n) {
+            R A[9], B[9], eps;
+            load_pair<SOA>(a, i, A, B, eps);
+            Rec<R> r;
+            tl.comparison++;
+            if (comparison_phase1(A, B, eps, thread_scratch<R>(), r)) {
+                store_rec<SOA>(a, i, r);
+                tl.result(r);
+                need2 = a.ids != nullptr;
+                e2 = i | IDS_ONLY;
+            } else {
+                need2 = true;
+                e2 = i;
+            }
+        }
+        push(Q.q2, &Q.n2, need2, e2);
+        __syncthreads();
+        drain<SOA, R>(a, Q, tl, false, 0u);
     }
+    drain<SOA, R>(a, Q, tl, true, 0u);
     // comparison_batch alone counts as comparison work but not as a fallback
     tl.flush<false>(a.stats);
 }
 
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK) iterative_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BLOCK, TC_ITER_MINB) iterative_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     const KP<R> kp = make_kp<R>(a);
     Tally tl;
     for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BLOCK) {
-        R A[9], B[9];
-        load_tri<SOA>(a.tri_a, i, a.n, A);
-        load_tri<SOA>(a.tri_b, i, a.n, B);
-        const R eps = R(a.eps ? a.eps[i] : a.eps_scalar);
+        R A[9], B[9], eps;
+        load_pair<SOA>(a, i, A, B, eps);
         Rec<R> r;
-        iterative_pair(A, B, eps, kp, r);
+        run_iterative<SOA>(a, i, A, B, eps, kp, r);
         store_rec<SOA>(a, i, r);
         tl.iterative++;
         tl.result(r);
@@ -211,42 +369,28 @@ __global__ void __launch_bounds__(BLOCK) iterative_kernel(Args<T> a) {
     tl.flush<false>(a.stats);
 }
 
+// RK/kernels.py:568-605.  Per tile of BLOCK pairs: the iterative kernel on
+// every lane; open (NOT_TERMINATED, fallback allowed, non-degenerate) pairs
+// are appended to q1; full batches of q1 run phase 1 of the comparison
+// kernel and non-intersecting ones move on to q2 for phase 2 -- so both
+// fallback phases execute on full warps, inside this kernel.
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK, 2) hybrid_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
-    __shared__ int64_t queue[2 * BLOCK];
-    __shared__ int qn;
+    __shared__ Queues Q;
     const KP<R> kp = make_kp<R>(a);
     Tally tl;
-    if (threadIdx.x == 0) qn = 0;
+    if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
     const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
-
-    auto fallback = [&](int64_t j) {
-        R A[9], B[9];
-        load_tri<SOA>(a.tri_a, j, a.n, A);
-        load_tri<SOA>(a.tri_b, j, a.n, B);
-        const R eps = R(a.eps ? a.eps[j] : a.eps_scalar);
-        Rec<R> r;
-        comparison_pair(A, B, eps, a.ids != nullptr, r);
-        // the pair was open (not settled) in the iterative pass
-        r.ids |= (uint32_t)FLAG_FALLBACK << 24;
-        store_rec<SOA>(a, j, r);
-        tl.comparison++;
-        tl.result(r);
-    };
-
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t i = tile * BLOCK + threadIdx.x;
         bool enq = false;
         if (i < a.n) {
-            R A[9], B[9];
-            load_tri<SOA>(a.tri_a, i, a.n, A);
-            load_tri<SOA>(a.tri_b, i, a.n, B);
-            const R eps = R(a.eps ? a.eps[i] : a.eps_scalar);
+            R A[9], B[9], eps;
+            load_pair<SOA>(a, i, A, B, eps);
             Rec<R> r;
-            iterative_pair(A, B, eps, kp, r);
+            run_iterative<SOA>(a, i, A, B, eps, kp, r);
             tl.iterative++;
             if (r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i])) {
                 if (degenerate_tri(A) || degenerate_tri(B)) {
@@ -262,26 +406,11 @@ __global__ void __launch_bounds__(BLOCK, 2) hybrid_kernel(Args<T> a) {
                 tl.result(r);
             }
         }
-        // warp-aggregated append to the block queue
-        const unsigned m = __ballot_sync(0xffffffffu, enq);
-        if (m) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(&qn, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (enq) queue[base + __popc(m & ((1u << lane) - 1u))] = i;
-        }
+        push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
-        const int q = qn;
-        if (q >= BLOCK) {
-            // a full block of open pairs: every thread takes one
-            fallback(queue[q - BLOCK + threadIdx.x]);
-            __syncthreads();
-            if (threadIdx.x == 0) qn = q - BLOCK;
-        }
-        __syncthreads();
+        drain<SOA, R>(a, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
-    const int q = qn;
-    if (threadIdx.x < q) fallback(queue[threadIdx.x]);
+    drain<SOA, R>(a, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     tl.flush<true>(a.stats);
 }
 
@@ -352,9 +481,9 @@ static int sm_count() {
 }
 
 template <typename K>
-static int64_t grid_for(K kernel, int64_t n) {
+static int64_t grid_for(K kernel, int64_t n, size_t smem = 0) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, 0) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     const int64_t tiles = (n + BLOCK - 1) / BLOCK;
     const int64_t full = (int64_t)sm_count() * per_sm;
@@ -365,15 +494,16 @@ enum Variant { V_COMPARISON = 0, V_ITERATIVE = 1, V_HYBRID = 2 };
 
 template <typename T, bool STRICT, bool SOA>
 static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
+    const size_t smem = scratch_bytes<T>();  // crossing-point scratch of the comparison phases
     if (variant == V_COMPARISON) {
         auto k = comparison_kernel<T, STRICT, SOA>;
-        k<<<(unsigned)grid_for(k, a.n), BLOCK, 0, s>>>(a);
+        k<<<(unsigned)grid_for(k, a.n, smem), BLOCK, smem, s>>>(a);
     } else if (variant == V_ITERATIVE) {
         auto k = iterative_kernel<T, STRICT, SOA>;
         k<<<(unsigned)grid_for(k, a.n), BLOCK, 0, s>>>(a);
     } else {
         auto k = hybrid_kernel<T, STRICT, SOA>;
-        k<<<(unsigned)grid_for(k, a.n), BLOCK, 0, s>>>(a);
+        k<<<(unsigned)grid_for(k, a.n, smem), BLOCK, smem, s>>>(a);
     }
     g_launches++;
     const cudaError_t e = cudaGetLastError();
