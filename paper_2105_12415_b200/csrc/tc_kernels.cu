@@ -105,7 +105,7 @@ __device__ __forceinline__ void run_iterative(const Args<T>& a, int64_t i, const
     if constexpr (IsStrict<R>::value) {
         iterative_pair(A, B, eps, kp, r, [&](R* A0, R* B0) { load_base<SOA>(a, i, A0, B0); });
     } else {
-        iterative_pair_gram(A, B, eps, kp, r, [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4) {
+        auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4) {
             R At[9], Bt[9];
             load_tri<SOA>(a.tri_a, i, a.n, At);
             load_tri<SOA>(a.tri_b, i, a.n, Bt);
@@ -118,7 +118,9 @@ __device__ __forceinline__ void run_iterative(const Args<T>& a, int64_t i, const
                 E3[k] = Bt[k] - Bt[3 + k];
                 E4[k] = Bt[k] - Bt[6 + k];
             }
-        });
+        };
+        if (kp.start_coord >= R(0) && kp.start_coord <= R(1)) iterative_pair_gram<true>(A, B, eps, kp, r, reload);
+        else iterative_pair_gram<false>(A, B, eps, kp, r, reload);
     }
 }
 
@@ -235,8 +237,25 @@ __device__ __forceinline__ Scratch<R> thread_scratch() {
     s.stride = BLOCK;
     return s;
 }
+// The calling thread's planar shared-memory slot for the pair under
+// comparison (18 coordinates, stride BLOCK), after the crossing scratch.
+template <bool SOA, class R, typename T>
+__device__ __forceinline__ void stage_pair(const Args<T>& a, int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) {
+    extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
+    T* slot = reinterpret_cast<T*>(tc_dyn_smem) + 18 * BLOCK + threadIdx.x;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        slot[k * BLOCK] = __ldg(SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
+        slot[(9 + k) * BLOCK] = __ldg(SOA ? a.tri_b + k * a.n + j : a.tri_b + 9 * j + k);
+    }
+    A.p = slot;
+    A.stride = BLOCK;
+    B.p = slot + 9 * BLOCK;
+    B.stride = BLOCK;
+    eps = R(a.eps ? a.eps[j] : a.eps_scalar);
+}
 template <typename T>
-constexpr size_t scratch_bytes() { return sizeof(T) * 18 * BLOCK; }
+constexpr size_t scratch_bytes() { return sizeof(T) * 36 * BLOCK; }
 constexpr int64_t IDS_ONLY = int64_t(1) << 62;
 
 // Warp-aggregated append (all 32 lanes of the warp must call it).
@@ -283,8 +302,9 @@ __device__ __forceinline__ void drain(const Args<T>& a, Queues& Q, Tally& tl, bo
         int64_t e2 = 0;
         if (e >= 0) {
             const int64_t j = e & (IDS_ONLY - 1);
-            R A[9], B[9], eps;
-            load_pair<SOA>(a, j, A, B, eps);
+            SmemTri<R> A, B;
+            R eps;
+            stage_pair<SOA>(a, j, A, B, eps);
             Rec<R> r;
             if (which == 1) {
                 tl.comparison++;
@@ -329,8 +349,9 @@ __global__ void __launch_bounds__(BLOCK, 2) comparison_kernel(Args<T> a) {
         bool need2 = false;
         int64_t e2 = 0;
         if (i < a.n) {
-            R A[9], B[9], eps;
-            load_pair<SOA>(a, i, A, B, eps);
+            SmemTri<R> A, B;
+            R eps;
+            stage_pair<SOA>(a, i, A, B, eps);
             Rec<R> r;
             tl.comparison++;
             if (comparison_phase1(A, B, eps, thread_scratch<R>(), r)) {
@@ -482,6 +503,11 @@ static int sm_count() {
 
 template <typename K>
 static int64_t grid_for(K kernel, int64_t n, size_t smem = 0) {
+    if (smem > 48 * 1024) {
+        // opt in to > 48 KB of dynamic shared memory (once per kernel is enough,
+        // but the call is cheap and idempotent)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;

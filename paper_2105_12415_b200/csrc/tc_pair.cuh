@@ -9,6 +9,17 @@
 
 namespace tc {
 
+// Unrolling of the comparison kernel's crossing (X) and feature (F) test
+// loops: full unrolling makes every vertex index a compile-time constant.
+#ifndef TC_UNROLL_X
+#define TC_UNROLL_X 1
+#endif
+#ifndef TC_UNROLL_F
+#define TC_UNROLL_F 1
+#endif
+constexpr int kUnrollX = TC_UNROLL_X;
+constexpr int kUnrollF = TC_UNROLL_F;
+
 enum : int { KIND_NO_CONTACT = 0, KIND_CONTACT = 1, KIND_NOT_TERMINATED = 2, KIND_DEGENERATE = 3 };
 
 // ids byte 3 flag bits
@@ -78,11 +89,11 @@ __device__ __forceinline__ bool degenerate_tri(const R* t) {
 // denominator, so the divergent region cases cost one division pair for the
 // whole warp.  u, w are the weights along ab, ac; results are the
 // reference's bit for bit in strict mode.
-template <class R>
-__device__ __forceinline__ int closest_point_params(const R* p, const R* tri, R& u, R& w) {
-    const R* a = tri;
-    const R* b = tri + 3;
-    const R* c = tri + 6;
+template <class R, class Tri>
+__device__ __forceinline__ int closest_point_params_t(const R* p, const Tri& tri, R& u, R& w) {
+    R a[3], b[3], c[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) { a[i] = tri[i]; b[i] = tri[3 + i]; c[i] = tri[6 + i]; }
     R ab[3], ac[3], t3[3];
     sub3(b, a, ab);
     sub3(c, a, ac);
@@ -126,23 +137,17 @@ __device__ __forceinline__ int closest_point_params(const R* p, const R* tri, R&
     return region;
 }
 
-template <class R>
-__device__ __forceinline__ void bary_point(const R* tri, R u, R w, R* out) {
+template <class R, class Tri>
+__device__ __forceinline__ void bary_point_t(const Tri& tri, R u, R w, R* out) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const R ab = tri[3 + i] - tri[i];
-        const R ac = tri[6 + i] - tri[i];
-        out[i] = (tri[i] + u * ab) + w * ac;
+        const R a = tri[i];
+        const R ab = tri[3 + i] - a;
+        const R ac = tri[6 + i] - a;
+        out[i] = (a + u * ab) + w * ac;
     }
 }
 
-// Full RK/kernels.py:157-221 (closest point and weights); used by cpt_kernel.
-template <class R>
-__device__ __forceinline__ int closest_point_triangle(const R* p, const R* tri, R* closest, R& u, R& w) {
-    const int region = closest_point_params(p, tri, u, w);
-    bary_point(tri, u, w, closest);
-    return region;
-}
 
 __device__ __forceinline__ int edge_start(int k) { return k; }
 __device__ __forceinline__ int edge_end(int k) { return k == 2 ? 0 : k + 1; }
@@ -152,6 +157,44 @@ template <class R>
 __device__ __forceinline__ void vertex_sel(const R* t, int k, R* v) {
 #pragma unroll
     for (int i = 0; i < 3; ++i) v[i] = (k == 0) ? t[i] : ((k == 1) ? t[3 + i] : t[6 + i]);
+}
+
+// Triangle accessors for the comparison phases: register-resident (RegTri)
+// or one thread's planar shared-memory slot (SmemTri, coordinate k at
+// p[k * stride]) -- the latter keeps the 18 pair coordinates out of the
+// register file during the register-hungry feature tests.
+template <class R>
+struct RegTri {
+    const R* t;
+    __device__ __forceinline__ R operator[](int k) const { return t[k]; }
+    __device__ __forceinline__ void vertex(int k, R* v) const { vertex_sel(t, k, v); }
+};
+template <class R>
+struct SmemTri {
+    const typename Store<R>::type* p;
+    int stride;
+    __device__ __forceinline__ R operator[](int k) const { return R(p[k * stride]); }
+    __device__ __forceinline__ void vertex(int k, R* v) const {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) v[i] = R(p[(3 * k + i) * stride]);
+    }
+};
+
+template <class R>
+__device__ __forceinline__ int closest_point_params(const R* p, const R* tri, R& u, R& w) {
+    return closest_point_params_t(p, RegTri<R>{tri}, u, w);
+}
+template <class R>
+__device__ __forceinline__ void bary_point(const R* tri, R u, R w, R* out) {
+    bary_point_t(RegTri<R>{tri}, u, w, out);
+}
+
+// Full RK/kernels.py:157-221 (closest point and weights); used by cpt_kernel.
+template <class R>
+__device__ __forceinline__ int closest_point_triangle(const R* p, const R* tri, R* closest, R& u, R& w) {
+    const int region = closest_point_params_t(p, RegTri<R>{tri}, u, w);
+    bary_point_t(RegTri<R>{tri}, u, w, closest);
+    return region;
 }
 
 // RK/kernels.py:224-252 _closest_segment_segment.  The parameters s, t are
@@ -203,12 +246,16 @@ struct PlaneFrame {
     R nrm[3], uu, uv, vv, det_safe, rdet;
 };
 
-template <class R>
-__device__ __forceinline__ void plane_frame(const R* tri, PlaneFrame<R>& f) {
+template <class R, class Tri>
+__device__ __forceinline__ void plane_frame(const Tri& tri, PlaneFrame<R>& f) {
     const R tiny = R(Tiny<R>::v);
     R u[3], v[3];
-    sub3(tri + 3, tri, u);
-    sub3(tri + 6, tri, v);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const R a = tri[i];
+        u[i] = tri[3 + i] - a;
+        v[i] = tri[6 + i] - a;
+    }
     cross3(u, v, f.nrm);
     f.uu = dot3(u, u);
     f.uv = dot3(u, v);
@@ -219,12 +266,14 @@ __device__ __forceinline__ void plane_frame(const R* tri, PlaneFrame<R>& f) {
 }
 
 // One proper crossing test of segment [p, q] through the closed triangle.
-template <class R>
-__device__ __forceinline__ bool segment_crosses(const R* p, const R* q, const R* tri, const PlaneFrame<R>& f, R* x) {
-    R t3[3], u[3], v[3];
-    sub3(p, tri, t3);
+template <class R, class Tri>
+__device__ __forceinline__ bool segment_crosses(const R* p, const R* q, const Tri& tri, const PlaneFrame<R>& f, R* x) {
+    R t3[3], u[3], v[3], a[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) a[i] = tri[i];
+    sub3(p, a, t3);
     const R dp = dot3(t3, f.nrm);
-    sub3(q, tri, t3);
+    sub3(q, a, t3);
     const R dq = dot3(t3, f.nrm);
     const bool crossing = (dp * dq) < R(0);
     const R denom = dp - dq;
@@ -232,9 +281,12 @@ __device__ __forceinline__ bool segment_crosses(const R* p, const R* q, const R*
     sub3(q, p, t3);
 #pragma unroll
     for (int i = 0; i < 3; ++i) x[i] = p[i] + t * t3[i];
-    sub3(tri + 3, tri, u);
-    sub3(tri + 6, tri, v);
-    sub3(x, tri, t3);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        u[i] = tri[3 + i] - a[i];
+        v[i] = tri[6 + i] - a[i];
+    }
+    sub3(x, a, t3);
     const R wu = dot3(t3, u);
     const R wv = dot3(t3, v);
     const R b1 = divr(f.vv * wu - f.uv * wv, f.det_safe, f.rdet);
@@ -269,19 +321,19 @@ struct Scratch {
     }
 };
 
-template <class R>
-__device__ __forceinline__ bool comparison_phase1(const R* A, const R* B, R eps, Scratch<R> cpts, Rec<R>& o) {
+template <class R, class Tri>
+__device__ __forceinline__ bool comparison_phase1(const Tri& A, const Tri& B, R eps, Scratch<R> cpts, Rec<R>& o) {
     using T = typename Store<R>::type;
     int ck = 0;  // crossing test index of each list slot, 3 bits per slot
     int nv = 0;
     {
         PlaneFrame<R> fb;
         plane_frame(B, fb);
-#pragma unroll 1
+#pragma unroll kUnrollX
         for (int k = 0; k < 3; ++k) {
             R p[3], q[3], x[3];
-            vertex_sel(A, edge_start(k), p);
-            vertex_sel(A, edge_end(k), q);
+            A.vertex(edge_start(k), p);
+            A.vertex(edge_end(k), q);
             if (segment_crosses(p, q, B, fb, x)) {
                 cpts.put(nv, x);
                 ck |= k << (3 * nv);
@@ -290,11 +342,11 @@ __device__ __forceinline__ bool comparison_phase1(const R* A, const R* B, R eps,
         }
         PlaneFrame<R> fa;
         plane_frame(A, fa);
-#pragma unroll 1
+#pragma unroll kUnrollX
         for (int k = 0; k < 3; ++k) {
             R p[3], q[3], x[3];
-            vertex_sel(B, edge_start(k), p);
-            vertex_sel(B, edge_end(k), q);
+            B.vertex(edge_start(k), p);
+            B.vertex(edge_end(k), q);
             if (segment_crosses(p, q, A, fa, x)) {
                 cpts.put(nv, x);
                 ck |= (3 + k) << (3 * nv);
@@ -332,8 +384,8 @@ __device__ __forceinline__ bool comparison_phase1(const R* A, const R* B, R eps,
     o.distance = R(0);
 #pragma unroll
     for (int i = 0; i < 3; ++i) { o.pa[i] = mid[i]; o.pb[i] = mid[i]; }
-    closest_point_params(mid, A, o.ba[0], o.ba[1]);
-    closest_point_params(mid, B, o.bb[0], o.bb[1]);
+    closest_point_params_t(mid, A, o.ba[0], o.ba[1]);
+    closest_point_params_t(mid, B, o.bb[0], o.bb[1]);
     o.kind = (o.distance <= R(T(2)) * eps) ? KIND_CONTACT : KIND_NO_CONTACT;
     o.ids = ((uint32_t)bidx << 16) | ((uint32_t)FLAG_INTERSECT << 24);
     return true;
@@ -345,30 +397,30 @@ __device__ __forceinline__ bool comparison_phase1(const R* A, const R* B, R eps,
 // strict results stay bit-identical.  `o.ids` bytes 0-1 get the feature row
 // and its region / segment-branch code; with `ids_only` (an intersecting
 // pair whose ids were requested) nothing else is written.
-template <class R>
-__device__ __forceinline__ void comparison_phase2(const R* A, const R* B, R eps, bool ids_only, Rec<R>& o) {
+template <class R, class Tri>
+__device__ __forceinline__ void comparison_phase2(const Tri& A, const Tri& B, R eps, bool ids_only, Rec<R>& o) {
     using T = typename Store<R>::type;
     const R tiny = R(Tiny<R>::v);
     int best_row = 0, best_code = 0;
     R best = R(0), bp1 = R(0), bp2 = R(0);
     // (two loops with fixed source/target triangles: a runtime choice between
     // the A and B arrays would force them out of registers)
-#pragma unroll 1
+#pragma unroll kUnrollF
     for (int row = 0; row < 3; ++row) {
         R pt[3], u, w, cl[3], diff[3];
-        vertex_sel(A, row, pt);
-        const int reg = closest_point_params(pt, B, u, w);
-        bary_point(B, u, w, cl);
+        A.vertex(row, pt);
+        const int reg = closest_point_params_t(pt, B, u, w);
+        bary_point_t(B, u, w, cl);
         sub3(pt, cl, diff);
         const R d2 = dot3(diff, diff);
         if (row == 0 || d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
     }
-#pragma unroll 1
+#pragma unroll kUnrollF
     for (int row = 3; row < 6; ++row) {
         R pt[3], u, w, cl[3], diff[3];
-        vertex_sel(B, row - 3, pt);
-        const int reg = closest_point_params(pt, A, u, w);
-        bary_point(A, u, w, cl);
+        B.vertex(row - 3, pt);
+        const int reg = closest_point_params_t(pt, A, u, w);
+        bary_point_t(A, u, w, cl);
         sub3(pt, cl, diff);
         const R d2 = dot3(diff, diff);
         if (d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
@@ -378,25 +430,25 @@ __device__ __forceinline__ void comparison_phase2(const R* A, const R* B, R eps,
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         R p[3], q[3], d[3];
-        vertex_sel(A, edge_start(k), p);
-        vertex_sel(A, edge_end(k), q);
+        A.vertex(edge_start(k), p);
+        A.vertex(edge_end(k), q);
         sub3(q, p, d);
         R l = dot3(d, d);
         ra[k] = rcpv(l > tiny ? l : R(1));
-        vertex_sel(B, edge_start(k), p);
-        vertex_sel(B, edge_end(k), q);
+        B.vertex(edge_start(k), p);
+        B.vertex(edge_end(k), q);
         sub3(q, p, d);
         l = dot3(d, d);
         rb[k] = rcpv(l > tiny ? l : R(1));
     }
-#pragma unroll 1
+#pragma unroll kUnrollF
     for (int row = 6; row < 15; ++row) {
         const int ka = (row - 6) / 3, kb = (row - 6) % 3;
         R p1[3], q1[3], p2[3], q2[3], s, t, d2;
-        vertex_sel(A, edge_start(ka), p1);
-        vertex_sel(A, edge_end(ka), q1);
-        vertex_sel(B, edge_start(kb), p2);
-        vertex_sel(B, edge_end(kb), q2);
+        A.vertex(edge_start(ka), p1);
+        A.vertex(edge_end(ka), q1);
+        B.vertex(edge_start(kb), p2);
+        B.vertex(edge_end(kb), q2);
         const R rak = (ka == 0) ? ra[0] : ((ka == 1) ? ra[1] : ra[2]);
         const R rbk = (kb == 0) ? rb[0] : ((kb == 1) ? rb[1] : rb[2]);
         const int code = segment_params(p1, q1, p2, q2, rak, rbk, s, t, d2);
@@ -406,24 +458,24 @@ __device__ __forceinline__ void comparison_phase2(const R* A, const R* B, R eps,
     if (ids_only) return;
     o.distance = sqrtv(best);
     if (best_row < 3) {
-        vertex_sel(A, best_row, o.pa);
-        bary_point(B, bp1, bp2, o.pb);
+        A.vertex(best_row, o.pa);
+        bary_point_t(B, bp1, bp2, o.pb);
         o.ba[0] = (best_row == 1) ? R(1) : R(0);
         o.ba[1] = (best_row == 2) ? R(1) : R(0);
         o.bb[0] = bp1; o.bb[1] = bp2;
     } else if (best_row < 6) {
-        bary_point(A, bp1, bp2, o.pa);
-        vertex_sel(B, best_row - 3, o.pb);
+        bary_point_t(A, bp1, bp2, o.pa);
+        B.vertex(best_row - 3, o.pb);
         o.ba[0] = bp1; o.ba[1] = bp2;
         o.bb[0] = (best_row == 4) ? R(1) : R(0);
         o.bb[1] = (best_row == 5) ? R(1) : R(0);
     } else {
         const int ka = (best_row - 6) / 3, kb = (best_row - 6) % 3;
         R p1[3], q1[3], p2[3], q2[3];
-        vertex_sel(A, edge_start(ka), p1);
-        vertex_sel(A, edge_end(ka), q1);
-        vertex_sel(B, edge_start(kb), p2);
-        vertex_sel(B, edge_end(kb), q2);
+        A.vertex(edge_start(ka), p1);
+        A.vertex(edge_end(ka), q1);
+        B.vertex(edge_start(kb), p2);
+        B.vertex(edge_end(kb), q2);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             o.pa[i] = p1[i] + bp1 * (q1[i] - p1[i]);
@@ -601,7 +653,7 @@ __device__ __forceinline__ void iterative_pair(const R* A, const R* B, R eps, co
 // slide gradients follow from e3a = E1 - E0 and -e3b = E4 - E3.  d itself
 // is rebuilt exactly from x where the settle test needs it.  Equal to the
 // reference up to rounding (checked within the north-star tolerance).
-template <class R, class Reload>
+template <bool BOX, class R, class Reload>
 __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R eps, const KP<R>& kp, Rec<R>& o,
                                                     Reload reload) {
     using T = typename Store<R>::type;
@@ -640,9 +692,10 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R ep
         for (int i = 0; i < 3; ++i) d[i] = (A[i] - B[i]) + x0 * E0[i] + x1 * E1[i] + x2 * E3[i] + x3 * E4[i];
         g0 = dot3(d, E0); g1 = dot3(d, E1); g3 = dot3(d, E3); g4 = dot3(d, E4);
     }
-    const bool box = kp.start_coord >= R(0) && kp.start_coord <= R(1);
-    auto hi_of = [&](R xp) { return box ? R(1) - xp : maxv(R(0), R(1) - maxv(xp, R(0))); };
-    auto clip_lo0 = [&](R v, R hi) { return box ? clip0_hi(v, hi) : clipv(v, R(0), hi); };
+    // BOX (start_coord in [0, 1], the usual case): the iterates never leave
+    // the box, so the inner max() of the clips are identities (coord_step)
+    auto hi_of = [&](R xp) { return BOX ? R(1) - xp : maxv(R(0), R(1) - maxv(xp, R(0))); };
+    auto clip_lo0 = [&](R v, R hi) { return BOX ? clip0_hi(v, hi) : clipv(v, R(0), hi); };
     auto sweep = [&]() {
         R t, s;
         t = clip_lo0(x0 - g0 * r0, hi_of(x1));
@@ -652,7 +705,7 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R ep
         s = t - x1; x1 = t;
         g0 += s * G01; g1 += s * G11; g3 += s * G13; g4 += s * G14;
         t = -(g1 - g0) * r3a;
-        t = box ? clipv(t, negv(x1), x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
+        t = BOX ? clipv(t, negv(x1), x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
         x0 = x0 - t; x1 = x1 + t;
         g0 += t * SA0; g1 += t * SA1; g3 += t * SA3; g4 += t * SA4;
         t = clip_lo0(x2 - g3 * r2, hi_of(x3));
@@ -662,7 +715,7 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R ep
         s = t - x3; x3 = t;
         g0 += s * G04; g1 += s * G14; g3 += s * G34; g4 += s * G44;
         t = -(g4 - g3) * r3b;
-        t = box ? clipv(t, negv(x3), x2) : clipv(t, -maxv(x3, R(0)), maxv(x2, R(0)));
+        t = BOX ? clipv(t, negv(x3), x2) : clipv(t, -maxv(x3, R(0)), maxv(x2, R(0)));
         x2 = x2 - t; x3 = x3 + t;
         g0 += t * SB0; g1 += t * SB1; g3 += t * SB3; g4 += t * SB4;
     };

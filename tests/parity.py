@@ -68,9 +68,10 @@ def compare_fast(O, variant, A, B, pkw, got, dtype, max_excused=None):
     n = len(A)
     p = O.make_params(**pkw)
     eps = np.full(n, p.epsilon, dtype)
-    cm = O.comparison(A, B, eps, dtype)
-    it = O.iterative(A, B, p, eps, dtype)
-    mg = O.margins(A, B, p, eps, dtype)
+    th = O.default_threads()
+    cm = O.comparison(A, B, eps, dtype, threads=th)
+    it = O.iterative(A, B, p, eps, dtype, threads=th)
+    mg = O.margins(A, B, p, eps, dtype, threads=th)
     L = longest_edge(A, B)
     L2 = L * L
     t_feat = mg[:, 0] <= tau * L2

@@ -154,3 +154,91 @@ def test_degenerate_fallback_marks_pairs():
     if hy["kind"][1] == 3:
         assert st["degenerate"] == 1
     assert not (hy["kind"] == 2).any()
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json config 1 scale (2^24 pairs): size-independent properties,
+# sampled bit-exact parity, and the fast build against the oracle on 2^20
+# pairs with the tie classifier.
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def cfg1():
+    A, B = W.random_pairs(1 << 24, seed=0, sep=(-0.1, 0.5))
+    planes = torch.from_numpy(W.to_soa(A, B)).cuda()
+    return A, B, planes
+
+
+@pytest.mark.slow
+def test_cfg1_strict_sampled_bitwise_and_stats(oracle_lib, cfg1):
+    A, B, planes = cfg1
+    n = A.shape[0]
+    p = D.Params(**PARAM_SETS["bl"])
+    stats = D.new_stats()
+    out = D.run("hybrid", planes[:9], planes[9:], p, soa=True, strict=True, ids=True, stats=stats, n=n)
+    torch.cuda.synchronize()
+    st = D.read_stats(stats)
+    kind = out["kind"].cpu().numpy()
+    ids = out["ids"].cpu().numpy()
+    dist = out["distance"].cpu().numpy()
+    # size-independent properties of the hybrid (RK/kernels.py:568-605)
+    assert not (kind == 2).any()
+    assert st["iterative"] == n
+    assert st["fallback"] == st["comparison"] == int(((ids[:, 3] & 4) > 0).sum())
+    assert st["contacts"] == int((kind == 1).sum())
+    assert st["intersecting"] == int(((ids[:, 3] & 16) > 0).sum())
+    assert st["min_distance"] == float(dist.min())
+    assert np.all((dist == 0) == ((ids[:, 3] & 16) > 0) | (dist > 0))
+    # bit-exact on a random sample against the oracle
+    rng = np.random.default_rng(7)
+    idx = np.sort(rng.choice(n, 20000, replace=False))
+    ref, _, rc = oracle_lib.hybrid(A[idx], B[idx], oracle_lib.make_params(**PARAM_SETS["bl"]), 1e-6)
+    assert rc == 0
+    cols = {"distance": dist, "kind": kind}
+    for k in ("point_a", "point_b", "bary_a", "bary_b"):
+        cols[k] = out[k].cpu().numpy().T
+    for k, v in cols.items():
+        assert np.array_equal(v[idx], ref[k]), k
+    assert np.array_equal(ids[idx], ref["ids"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("strict", [True, False])
+def test_cfg1_shard_invariance(cfg1, strict):
+    """Contiguous shards give bit-identical results and summed stats."""
+    A, B, planes = cfg1
+    n = A.shape[0]
+    p = D.Params(**PARAM_SETS["bl"])
+    whole = D.new_stats()
+    full = D.run("hybrid", planes[:9].contiguous(), planes[9:].contiguous(), p, soa=True, strict=strict,
+                 stats=whole, n=n)
+    parts = []
+    part_stats = []
+    for w in range(4):
+        lo, hi = w * n // 4, (w + 1) * n // 4
+        sub = planes[:, lo:hi].contiguous()
+        s = D.new_stats()
+        parts.append(D.run("hybrid", sub[:9], sub[9:], p, soa=True, strict=strict, stats=s, n=hi - lo))
+        part_stats.append(D.read_stats(s))
+    torch.cuda.synchronize()
+    for k in ("kind", "distance"):
+        assert torch.equal(full[k], torch.cat([q[k] for q in parts], dim=-1)), k
+    for k in ("point_a", "bary_b"):
+        assert torch.equal(full[k], torch.cat([q[k] for q in parts], dim=1)), k
+    ws = D.read_stats(whole)
+    for k in ("iterative", "comparison", "fallback", "contacts", "intersecting"):
+        assert ws[k] == sum(s[k] for s in part_stats), k
+    assert ws["min_distance"] == min(s["min_distance"] for s in part_stats)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_fast_vs_oracle_one_million(oracle_lib, real):
+    """The fast build on 2^20 fresh pairs (chunks 256..511 of cfg1) within tolerance."""
+    dt = DTYPES[real]
+    A, B = W.random_pairs(1 << 20, seed=0, sep=(-0.1, 0.5), start=1 << 20)
+    A = A.astype(dt)
+    B = B.astype(dt)
+    got, _ = run_dev("hybrid", A, B, real, "bl", False)
+    rep = parity.compare_fast(oracle_lib, "hybrid", A, B, PARAM_SETS["bl"], got, dt)
+    assert rep["ok"], rep
