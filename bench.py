@@ -47,9 +47,16 @@ METRIC = "triangle-pair contact queries/sec (hybrid, fp64)"
 UNIT = "pairs/s"
 
 
-def flops_per_launch(n, n_it, fallback, intersecting):
+def flops_reference_model(n, n_it, fallback, intersecting):
     """200 + 88 N per pair, +1199 per fallback, +254 if it intersects."""
     return n * (200 + 88 * n_it) + 1199 * fallback + 254 * intersecting
+
+
+def flops_executed(n, n_it, fallback, intersecting):
+    """The algorithm this kernel executes: an intersecting fallback pair runs the
+    six edge-plane tests (268) and the crossing resolution (254) but not the 15
+    feature tests, whose results it does not use (931 of the 1199)."""
+    return n * (200 + 88 * n_it) + 1199 * (fallback - intersecting) + (268 + 254) * intersecting
 
 
 # ---------------------------------------------------------------------------
@@ -243,7 +250,8 @@ def main():
     n_local = n
     fb_local = st["fallback"] / world
     fbx_local = st["intersecting"] / world
-    flops = flops_per_launch(n_local, PARAMS["n_iterative"], fb_local, fbx_local)
+    flops = flops_executed(n_local, PARAMS["n_iterative"], fb_local, fbx_local)
+    flops_ref = flops_reference_model(n_local, PARAMS["n_iterative"], fb_local, fbx_local)
     achieved_tf = flops / (ms_kernel / 1e3) / 1e12
     sink = torch.empty(4096, dtype=torch.float64, device=dev)
     blocks = 148 * 8
@@ -266,19 +274,25 @@ def main():
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     traffic = None
+    traffic_note = None
     prof = ROOT / "profiles" / "ncu_hybrid_f64_summary.json"
     if prof.exists():
         try:
             pj = json.loads(prof.read_text())
             if pj.get("n") == n_local:
                 traffic = pj.get("dram_bytes_per_launch")
+                traffic_note = pj.get("source")
         except ValueError:
             pass
     roofline = {
         "bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
-        "traffic": traffic,
+        "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
+        "traffic_source": traffic_note, "algorithmic_bytes_per_launch": n_local * 233,
         "kernel": "hybrid_kernel<double,fast,soa>", "kernel_ms": ms_kernel,
-        "flops_per_launch": flops, "flop_model": "SURVEY.md App. A: n(200+88N) + 1199 fallback + 254 fallback&intersect",
+        "flops_per_launch": flops,
+        "flop_model": "executed: n(200+88N) + 1199 (fallback - fallback&intersect) + 522 fallback&intersect "
+                      "(SURVEY.md App. A counts; intersecting fallbacks skip the 15 feature tests)",
+        "reference_model_tflops": flops_ref / (ms_kernel / 1e3) / 1e12,
         "peak_source": "in-run DFMA probe (tc_fma_probe); MEASURED_PEAKS.json has no FP64 figure",
         "hbm": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
                 "bytes_per_pair": bytes_per_pair, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},

@@ -87,36 +87,50 @@ __device__ __forceinline__ void load_tri(const T* __restrict__ src, int64_t i, i
     }
 }
 
-// Base vertices (v0 of A and B) of pair i, re-read after the sweep loop.
-template <bool SOA, class R, typename T>
-__device__ __forceinline__ void load_base(const Args<T>& a, int64_t i, R* A0, R* B0) {
+// The calling thread's planar shared-memory slot of 18 pair coordinates
+// (stride BLOCK, conflict-free), `offset` elements into the dynamic smem.
+template <typename T>
+__device__ __forceinline__ T* thread_slot(int offset) {
+    extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
+    return reinterpret_cast<T*>(tc_dyn_smem) + offset + threadIdx.x;
+}
+
+// Keep the register-resident pair in the thread's slot so the iterative
+// epilogue re-reads it from shared memory instead of global memory.
+template <class R, typename T>
+__device__ __forceinline__ void stash_pair(T* slot, const R* A, const R* B) {
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        A0[k] = R(__ldg(SOA ? a.tri_a + k * a.n + i : a.tri_a + 9 * i + k));
-        B0[k] = R(__ldg(SOA ? a.tri_b + k * a.n + i : a.tri_b + 9 * i + k));
+    for (int k = 0; k < 9; ++k) {
+        slot[k * BLOCK] = val(A[k]);
+        slot[(9 + k) * BLOCK] = val(B[k]);
     }
 }
 
 // Iterative kernel for one pair: the reference's operation order in strict
-// mode, the Gram-matrix form in the fast build (tc_pair.cuh).
-template <bool SOA, class R, typename T>
-__device__ __forceinline__ void run_iterative(const Args<T>& a, int64_t i, const R* A, const R* B, R eps,
-                                              const KP<R>& kp, Rec<R>& r) {
+// mode, the Gram-matrix form in the fast build (tc_pair.cuh).  `slot` holds
+// the pair (stash_pair) for the epilogue's re-reads.
+template <class R, typename T>
+__device__ __forceinline__ void run_iterative(const T* slot, const R* A, const R* B, R eps, const KP<R>& kp,
+                                              Rec<R>& r) {
     if constexpr (IsStrict<R>::value) {
-        iterative_pair(A, B, eps, kp, r, [&](R* A0, R* B0) { load_base<SOA>(a, i, A0, B0); });
-    } else {
-        auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4) {
-            R At[9], Bt[9];
-            load_tri<SOA>(a.tri_a, i, a.n, At);
-            load_tri<SOA>(a.tri_b, i, a.n, Bt);
+        iterative_pair(A, B, eps, kp, r, [&](R* A0, R* B0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                A0[k] = At[k];
-                B0[k] = Bt[k];
-                E0[k] = At[3 + k] - At[k];
-                E1[k] = At[6 + k] - At[k];
-                E3[k] = Bt[k] - Bt[3 + k];
-                E4[k] = Bt[k] - Bt[6 + k];
+                A0[k] = R(slot[k * BLOCK]);
+                B0[k] = R(slot[(9 + k) * BLOCK]);
+            }
+        });
+    } else {
+        auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const R a0 = R(slot[k * BLOCK]), b0 = R(slot[(9 + k) * BLOCK]);
+                A0[k] = a0;
+                B0[k] = b0;
+                E0[k] = R(slot[(3 + k) * BLOCK]) - a0;
+                E1[k] = R(slot[(6 + k) * BLOCK]) - a0;
+                E3[k] = b0 - R(slot[(12 + k) * BLOCK]);
+                E4[k] = b0 - R(slot[(15 + k) * BLOCK]);
             }
         };
         if (kp.start_coord >= R(0) && kp.start_coord <= R(1)) iterative_pair_gram<true>(A, B, eps, kp, r, reload);
@@ -241,8 +255,7 @@ __device__ __forceinline__ Scratch<R> thread_scratch() {
 // comparison (18 coordinates, stride BLOCK), after the crossing scratch.
 template <bool SOA, class R, typename T>
 __device__ __forceinline__ void stage_pair(const Args<T>& a, int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) {
-    extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
-    T* slot = reinterpret_cast<T*>(tc_dyn_smem) + 18 * BLOCK + threadIdx.x;
+    T* slot = thread_slot<T>(18 * BLOCK);
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
         slot[k * BLOCK] = __ldg(SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
@@ -381,8 +394,10 @@ __global__ void __launch_bounds__(BLOCK, TC_ITER_MINB) iterative_kernel(Args<T> 
     for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BLOCK) {
         R A[9], B[9], eps;
         load_pair<SOA>(a, i, A, B, eps);
+        T* slot = thread_slot<T>(0);
+        stash_pair(slot, A, B);
         Rec<R> r;
-        run_iterative<SOA>(a, i, A, B, eps, kp, r);
+        run_iterative(slot, A, B, eps, kp, r);
         store_rec<SOA>(a, i, r);
         tl.iterative++;
         tl.result(r);
@@ -394,7 +409,10 @@ __global__ void __launch_bounds__(BLOCK, TC_ITER_MINB) iterative_kernel(Args<T> 
 // every lane; open (NOT_TERMINATED, fallback allowed, non-degenerate) pairs
 // are appended to q1; full batches of q1 run phase 1 of the comparison
 // kernel and non-intersecting ones move on to q2 for phase 2 -- so both
-// fallback phases execute on full warps, inside this kernel.
+// fallback phases execute on full warps, inside this kernel.  (Running
+// phase 1 in-tile on the compacted open lanes, straight from the owners'
+// shared-memory slots, saves the re-read of queued pairs but idles half the
+// warps: measured 8% slower on cfg1.)
 template <typename T, bool STRICT, bool SOA>
 __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
@@ -410,8 +428,10 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
         if (i < a.n) {
             R A[9], B[9], eps;
             load_pair<SOA>(a, i, A, B, eps);
+            T* slot = thread_slot<T>(18 * BLOCK);  // the comparison phases' pair slot, free here
+            stash_pair(slot, A, B);
             Rec<R> r;
-            run_iterative<SOA>(a, i, A, B, eps, kp, r);
+            run_iterative(slot, A, B, eps, kp, r);
             tl.iterative++;
             if (r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i])) {
                 if (degenerate_tri(A) || degenerate_tri(B)) {
@@ -422,10 +442,10 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
                     enq = true;
                 }
             }
-            if (!enq) {
-                store_rec<SOA>(a, i, r);
-                tl.result(r);
-            }
+            // every lane stores its tile result now (open pairs a placeholder
+            // the fallback overwrites), so output sectors are written whole
+            store_rec<SOA>(a, i, r);
+            if (!enq) tl.result(r);
         }
         push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
@@ -526,7 +546,8 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         k<<<(unsigned)grid_for(k, a.n, smem), BLOCK, smem, s>>>(a);
     } else if (variant == V_ITERATIVE) {
         auto k = iterative_kernel<T, STRICT, SOA>;
-        k<<<(unsigned)grid_for(k, a.n), BLOCK, 0, s>>>(a);
+        const size_t ism = sizeof(T) * 18 * BLOCK;  // the pair slot of the epilogue re-reads
+        k<<<(unsigned)grid_for(k, a.n, ism), BLOCK, ism, s>>>(a);
     } else {
         auto k = hybrid_kernel<T, STRICT, SOA>;
         k<<<(unsigned)grid_for(k, a.n, smem), BLOCK, smem, s>>>(a);
