@@ -166,7 +166,9 @@ __device__ __forceinline__ void store_rec(const Args<T>& a, int64_t i, const Rec
 
 // ---- per-CTA tallies -> tc_stats ----------------------------------------------
 struct Tally {
-    unsigned long long iterative = 0, comparison = 0, degenerate = 0, contacts = 0, intersecting = 0;
+    // per-thread counts fit 32 bits (a thread sees at most n / (grid * BLOCK)
+    // pairs); widened to 64 bits in the CTA reduction
+    unsigned iterative = 0, comparison = 0, degenerate = 0, contacts = 0, intersecting = 0;
     double min_d = __builtin_huge_val();
 
     template <class R>
@@ -185,19 +187,21 @@ struct Tally {
         __shared__ unsigned long long red[5][BLOCK / 32];  // iterative, comparison, degenerate, contacts, intersecting
         __shared__ double redm[BLOCK / 32];
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        unsigned long long it64 = iterative, cm64 = comparison, dg64 = degenerate, ct64 = contacts,
+                           ix64 = intersecting;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            iterative += __shfl_xor_sync(0xffffffffu, iterative, off);
-            comparison += __shfl_xor_sync(0xffffffffu, comparison, off);
-            degenerate += __shfl_xor_sync(0xffffffffu, degenerate, off);
-            contacts += __shfl_xor_sync(0xffffffffu, contacts, off);
-            intersecting += __shfl_xor_sync(0xffffffffu, intersecting, off);
+            it64 += __shfl_xor_sync(0xffffffffu, it64, off);
+            cm64 += __shfl_xor_sync(0xffffffffu, cm64, off);
+            dg64 += __shfl_xor_sync(0xffffffffu, dg64, off);
+            ct64 += __shfl_xor_sync(0xffffffffu, ct64, off);
+            ix64 += __shfl_xor_sync(0xffffffffu, ix64, off);
             const double o = __shfl_xor_sync(0xffffffffu, min_d, off);
             min_d = (o < min_d) ? o : min_d;
         }
         if (lane == 0) {
-            red[0][wid] = iterative; red[1][wid] = comparison; red[2][wid] = degenerate; red[3][wid] = contacts;
-            red[4][wid] = intersecting;
+            red[0][wid] = it64; red[1][wid] = cm64; red[2][wid] = dg64; red[3][wid] = ct64;
+            red[4][wid] = ix64;
             redm[wid] = min_d;
         }
         __syncthreads();
@@ -434,7 +438,8 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
             run_iterative(slot, A, B, eps, kp, r);
             tl.iterative++;
             if (r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i])) {
-                if (degenerate_tri(A) || degenerate_tri(B)) {
+                const SmemTri<R> SA{slot, BLOCK}, SB{slot + 9 * BLOCK, BLOCK};
+                if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {
                     r.kind = KIND_DEGENERATE;
                     r.ids |= (uint32_t)FLAG_DEGENERATE << 24;
                     tl.degenerate++;

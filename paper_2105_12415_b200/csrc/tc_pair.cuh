@@ -180,6 +180,16 @@ struct SmemTri {
     }
 };
 
+// RK/geometry.py:68-75 degenerate_mask through an accessor (e.g. a pair kept
+// in shared memory, so the caller's registers are not pinned by it).
+template <class R, class Tri>
+__device__ __forceinline__ bool degenerate_tri_t(const Tri& t) {
+    R v[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = t[k];
+    return degenerate_tri(v);
+}
+
 template <class R>
 __device__ __forceinline__ int closest_point_params(const R* p, const R* tri, R& u, R& w) {
     return closest_point_params_t(p, RegTri<R>{tri}, u, w);
@@ -513,24 +523,70 @@ __device__ __forceinline__ void contact_mid(const R* A0, const R* x, const R* e1
     for (int i = 0; i < 3; ++i) m[i] = ((A0[i] + x[0] * e1a[i]) + x[1] * e2a[i]) - half * d[i];
 }
 
-// Fast-build helpers: the lower clip at 0 by the sign bit and negation by a
-// sign flip run on the integer pipe, leaving the FP64 pipe to arithmetic.
-__device__ __forceinline__ double clip0_hi(double x, double hi) {
-    x = (__double2hiint(x) < 0) ? 0.0 : x;
-    return (x < hi) ? x : hi;
-}
-__device__ __forceinline__ float clip0_hi(float x, float hi) {
-    x = (__float_as_int(x) < 0) ? 0.0f : x;
-    return (x < hi) ? x : hi;
-}
-template <typename T>
-__device__ __forceinline__ Strict<T> clip0_hi(Strict<T> x, Strict<T> hi) { return clipv(x, Strict<T>(0), hi); }
+// Clips.  A double compare (DSETP) plus its dependent select costs ~15-25
+// cycles of latency on B200 (tools/latency_probe.cu: DFMA + one min = 24
+// cycles, DFMA + a two-sided fmax/fmin clip = 58), and the iterative kernel
+// is one long chain of clips.  The lower clip at 0 is a sign-bit test on the
+// integer pipe.  TC_INT_CLIP=1 also does the upper compare on 64-bit integer
+// patterns (for non-negative IEEE values the patterns order like the values);
+// measured slower (9.2 vs 9.9 G pairs/s iterative), so it is off.
+// NaN inputs are not supported.
+//
+// clip0_hi(x, hi) == np.clip(x, 0, hi) bit for bit for hi >= +0 (x <= 0,
+// including -0, gives +0; ties give hi), so strict mode uses it too.
 __device__ __forceinline__ double negv(double x) {
     return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
 }
 __device__ __forceinline__ float negv(float x) { return __int_as_float(__float_as_int(x) ^ (int)0x80000000); }
 template <typename T>
 __device__ __forceinline__ Strict<T> negv(Strict<T> x) { return -x; }
+
+#ifndef TC_INT_CLIP
+#define TC_INT_CLIP 0
+#endif
+__device__ __forceinline__ double clip0_hi(double x, double hi) {
+#if TC_INT_CLIP
+    long long xb = __double_as_longlong(x);
+    const long long hb = __double_as_longlong(hi);
+    xb = (xb < 0) ? 0 : xb;
+    return __longlong_as_double(xb < hb ? xb : hb);
+#else
+    x = (__double2hiint(x) < 0) ? 0.0 : x;
+    return (x < hi) ? x : hi;
+#endif
+}
+__device__ __forceinline__ float clip0_hi(float x, float hi) {
+    int xb = __float_as_int(x);
+    const int hb = __float_as_int(hi);
+    xb = (xb < 0) ? 0 : xb;
+    return __int_as_float(xb < hb ? xb : hb);
+}
+template <typename T>
+__device__ __forceinline__ Strict<T> clip0_hi(Strict<T> x, Strict<T> hi) { return clip0_hi(x.v, hi.v); }
+
+// clip(t, -xb, xa) for xa, xb >= 0 (the fast build's box mode): clip the
+// magnitude against the bound on t's side, keep t's sign.
+__device__ __forceinline__ double clip_sym(double t, double xb, double xa) {
+#if !TC_INT_CLIP
+    t = (t > negv(xb)) ? t : negv(xb);
+    return (t < xa) ? t : xa;
+#endif
+    const long long tb = __double_as_longlong(t);
+    const long long mag = tb & 0x7FFFFFFFFFFFFFFFLL;
+    const long long lim = (tb < 0) ? __double_as_longlong(xb) : __double_as_longlong(xa);
+    const long long r = mag < lim ? mag : lim;
+    return __longlong_as_double(r | (tb & (long long)0x8000000000000000ULL));
+}
+__device__ __forceinline__ float clip_sym(float t, float xb, float xa) {
+    const int tb = __float_as_int(t);
+    const int mag = tb & 0x7FFFFFFF;
+    const int lim = (tb < 0) ? __float_as_int(xb) : __float_as_int(xa);
+    const int r = mag < lim ? mag : lim;
+    return __int_as_float(r | (tb & (int)0x80000000));
+}
+template <typename T>
+__device__ __forceinline__ Strict<T> clip_sym(Strict<T> t, Strict<T> xb, Strict<T> xa) { return clip_sym(t.v, xb.v, xa.v); }
+
 
 // One coordinate substep (RK/kernels.py:531-536): preconditioned descent on
 // the quadratic part, then the clip to [0, max(0, 1 - max(x_partner, 0))].
@@ -541,7 +597,7 @@ template <class R>
 __device__ __forceinline__ void coord_step(R& xk, R xp, const R* e, R den, R rcp, R* d, bool box) {
     R target = xk - divr(dot3(d, e), den, rcp);
     if (!IsStrict<R>::value && box) target = clip0_hi(target, R(1) - xp);
-    else target = clipv(target, R(0), maxv(R(0), R(1) - maxv(xp, R(0))));
+    else target = clip0_hi(target, maxv(R(0), R(1) - maxv(xp, R(0))));
     const R step = target - xk;
     xk = target;
 #pragma unroll
@@ -552,7 +608,7 @@ __device__ __forceinline__ void coord_step(R& xk, R xp, const R* e, R den, R rcp
 template <class R>
 __device__ __forceinline__ void slide_step(R& xa, R& xb, const R* e3, R den3, R rcp3, R* d, bool box) {
     R t = divr(-dot3(d, e3), den3, rcp3);
-    if (!IsStrict<R>::value && box) t = clipv(t, negv(xb), xa);
+    if (!IsStrict<R>::value && box) t = clip_sym(t, xb, xa);
     else t = clipv(t, -maxv(xb, R(0)), maxv(xa, R(0)));
     xa = xa - t;
     xb = xb + t;
@@ -695,7 +751,7 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R ep
     // BOX (start_coord in [0, 1], the usual case): the iterates never leave
     // the box, so the inner max() of the clips are identities (coord_step)
     auto hi_of = [&](R xp) { return BOX ? R(1) - xp : maxv(R(0), R(1) - maxv(xp, R(0))); };
-    auto clip_lo0 = [&](R v, R hi) { return BOX ? clip0_hi(v, hi) : clipv(v, R(0), hi); };
+    auto clip_lo0 = [&](R v, R hi) { return clip0_hi(v, hi); };
     auto sweep = [&]() {
         R t, s;
         t = clip_lo0(x0 - g0 * r0, hi_of(x1));
@@ -705,7 +761,7 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R ep
         s = t - x1; x1 = t;
         g0 += s * G01; g1 += s * G11; g3 += s * G13; g4 += s * G14;
         t = -(g1 - g0) * r3a;
-        t = BOX ? clipv(t, negv(x1), x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
+        t = BOX ? clip_sym(t, x1, x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
         x0 = x0 - t; x1 = x1 + t;
         g0 += t * SA0; g1 += t * SA1; g3 += t * SA3; g4 += t * SA4;
         t = clip_lo0(x2 - g3 * r2, hi_of(x3));
@@ -715,7 +771,7 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R ep
         s = t - x3; x3 = t;
         g0 += s * G04; g1 += s * G14; g3 += s * G34; g4 += s * G44;
         t = -(g4 - g3) * r3b;
-        t = BOX ? clipv(t, negv(x3), x2) : clipv(t, -maxv(x3, R(0)), maxv(x2, R(0)));
+        t = BOX ? clip_sym(t, x3, x2) : clipv(t, -maxv(x3, R(0)), maxv(x2, R(0)));
         x2 = x2 - t; x3 = x3 + t;
         g0 += t * SB0; g1 += t * SB1; g3 += t * SB3; g4 += t * SB4;
     };
