@@ -551,8 +551,12 @@ __device__ __forceinline__ double clip0_hi(double x, double hi) {
     xb = (xb < 0) ? 0 : xb;
     return __longlong_as_double(xb < hb ? xb : hb);
 #else
-    x = (__double2hiint(x) < 0) ? 0.0 : x;
-    return (x < hi) ? x : hi;
+    // both tests read the unclipped x, so they issue in parallel (one compare
+    // latency on the chain instead of two); equal to min(max(x, 0), hi) for
+    // hi >= +0, including signed zeros
+    const bool neg = __double2hiint(x) < 0;
+    const double r = (x < hi) ? x : hi;
+    return neg ? 0.0 : r;
 #endif
 }
 __device__ __forceinline__ float clip0_hi(float x, float hi) {
@@ -568,8 +572,10 @@ __device__ __forceinline__ Strict<T> clip0_hi(Strict<T> x, Strict<T> hi) { retur
 // magnitude against the bound on t's side, keep t's sign.
 __device__ __forceinline__ double clip_sym(double t, double xb, double xa) {
 #if !TC_INT_CLIP
-    t = (t > negv(xb)) ? t : negv(xb);
-    return (t < xa) ? t : xa;
+    // independent compares of the unclipped t against both bounds
+    const double lo = negv(xb);
+    const bool below = !(t > lo), above = !(t < xa);
+    return below ? lo : (above ? xa : t);
 #endif
     const long long tb = __double_as_longlong(t);
     const long long mag = tb & 0x7FFFFFFFFFFFFFFFLL;
