@@ -62,8 +62,9 @@ struct Args {
     int n_iterative;
 };
 
-template <class R, typename T>
-__device__ __forceinline__ KP<R> make_kp(const Args<T>& a) {
+template <class R, class A>
+__device__ __forceinline__ KP<R> make_kp(const A& a) {
+    using T = typename Store<R>::type;
     KP<R> k;
     k.c_factor = R(T(a.c_factor));
     k.alpha_it = R(T(a.alpha_it));
@@ -107,35 +108,40 @@ __device__ __forceinline__ void stash_pair(T* slot, const R* A, const R* B) {
 }
 
 // Iterative kernel for one pair: the reference's operation order in strict
-// mode, the Gram-matrix form in the fast build (tc_pair.cuh).  `slot` holds
-// the pair (stash_pair) for the epilogue's re-reads.
-template <class R, typename T>
-__device__ __forceinline__ void run_iterative(const T* slot, const R* A, const R* B, R eps, const KP<R>& kp,
-                                              Rec<R>& r) {
+// mode, the Gram-matrix form in the fast build (tc_pair.cuh).  SA / SB give
+// the epilogue's re-reads of the pair (a shared-memory copy).
+template <class R, class TA, class TB>
+__device__ __forceinline__ void run_iterative(const TA& SA, const TB& SB, const R* A, const R* B, R eps,
+                                              const KP<R>& kp, Rec<R>& r) {
     if constexpr (IsStrict<R>::value) {
         iterative_pair(A, B, eps, kp, r, [&](R* A0, R* B0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                A0[k] = R(slot[k * BLOCK]);
-                B0[k] = R(slot[(9 + k) * BLOCK]);
+                A0[k] = SA[k];
+                B0[k] = SB[k];
             }
         });
     } else {
         auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                const R a0 = R(slot[k * BLOCK]), b0 = R(slot[(9 + k) * BLOCK]);
+                const R a0 = SA[k], b0 = SB[k];
                 A0[k] = a0;
                 B0[k] = b0;
-                E0[k] = R(slot[(3 + k) * BLOCK]) - a0;
-                E1[k] = R(slot[(6 + k) * BLOCK]) - a0;
-                E3[k] = b0 - R(slot[(12 + k) * BLOCK]);
-                E4[k] = b0 - R(slot[(15 + k) * BLOCK]);
+                E0[k] = SA[3 + k] - a0;
+                E1[k] = SA[6 + k] - a0;
+                E3[k] = b0 - SB[3 + k];
+                E4[k] = b0 - SB[6 + k];
             }
         };
         if (kp.start_coord >= R(0) && kp.start_coord <= R(1)) iterative_pair_gram<true>(A, B, eps, kp, r, reload);
         else iterative_pair_gram<false>(A, B, eps, kp, r, reload);
     }
+}
+template <class R, typename T>
+__device__ __forceinline__ void run_iterative(const T* slot, const R* A, const R* B, R eps, const KP<R>& kp,
+                                              Rec<R>& r) {
+    run_iterative(SmemTri<R>{slot, BLOCK}, SmemTri<R>{slot + 9 * BLOCK, BLOCK}, A, B, eps, kp, r);
 }
 
 template <bool SOA, class R, typename T>
@@ -293,12 +299,29 @@ __device__ __forceinline__ void load_pair(const Args<T>& a, int64_t j, R* A, R* 
     eps = R(a.eps ? a.eps[j] : a.eps_scalar);
 }
 
+// Where the comparison phases read a queued pair from and write its result
+// to.  FlatSource: pair j of the flat (n,3,3)/SoA batch, staged into the
+// thread's shared-memory slot; results into the BatchResult columns.
+template <bool SOA, class R, typename T>
+struct FlatSource {
+    const Args<T>& a;
+    __device__ __forceinline__ bool want_ids() const { return a.ids != nullptr; }
+    __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
+        stage_pair<SOA>(a, j, A, B, eps);
+    }
+    __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const { store_rec<SOA>(a, j, r); }
+    __device__ __forceinline__ void store_ids01(int64_t j, uint32_t ids) const {
+        a.ids[4 * j] = (uint8_t)(ids & 0xFF);
+        a.ids[4 * j + 1] = (uint8_t)((ids >> 8) & 0xFF);
+    }
+};
+
 // Run whole batches (BLOCK pairs, or the remainder when `final_`) from the
 // queues until neither holds a full batch.  Block-uniform; every batch runs
 // on full warps.  `fallback_flag`: hybrid results carry FLAG_FALLBACK.
-template <bool SOA, class R, typename T>
-__device__ __forceinline__ void drain(const Args<T>& a, Queues& Q, Tally& tl, bool final_, uint32_t fallback_flag) {
-    const bool want_ids = a.ids != nullptr;
+template <class R, class Src>
+__device__ __forceinline__ void drain(const Src& src, Queues& Q, Tally& tl, bool final_, uint32_t fallback_flag) {
+    const bool want_ids = src.want_ids();
     while (true) {
         const int c1 = Q.n1, c2 = Q.n2;
         __syncthreads();  // everyone has read the counts before they change
@@ -321,13 +344,13 @@ __device__ __forceinline__ void drain(const Args<T>& a, Queues& Q, Tally& tl, bo
             const int64_t j = e & (IDS_ONLY - 1);
             SmemTri<R> A, B;
             R eps;
-            stage_pair<SOA>(a, j, A, B, eps);
+            src.stage(j, A, B, eps);
             Rec<R> r;
             if (which == 1) {
                 tl.comparison++;
                 if (comparison_phase1(A, B, eps, thread_scratch<R>(), r)) {
                     r.ids |= fallback_flag << 24;
-                    store_rec<SOA>(a, j, r);
+                    src.store(j, r);
                     tl.result(r);
                     push2 = want_ids;
                     e2 = j | IDS_ONLY;
@@ -339,11 +362,10 @@ __device__ __forceinline__ void drain(const Args<T>& a, Queues& Q, Tally& tl, bo
                 const bool ids_only = (e & IDS_ONLY) != 0;
                 comparison_phase2(A, B, eps, ids_only, r);
                 if (ids_only) {
-                    a.ids[4 * j] = (uint8_t)(r.ids & 0xFF);
-                    a.ids[4 * j + 1] = (uint8_t)((r.ids >> 8) & 0xFF);
+                    src.store_ids01(j, r.ids);
                 } else {
                     r.ids |= fallback_flag << 24;
-                    store_rec<SOA>(a, j, r);
+                    src.store(j, r);
                     tl.result(r);
                 }
             }
@@ -383,9 +405,9 @@ __global__ void __launch_bounds__(BLOCK, 2) comparison_kernel(Args<T> a) {
         }
         push(Q.q2, &Q.n2, need2, e2);
         __syncthreads();
-        drain<SOA, R>(a, Q, tl, false, 0u);
+        drain<R>(FlatSource<SOA, R, T>{a}, Q, tl, false, 0u);
     }
-    drain<SOA, R>(a, Q, tl, true, 0u);
+    drain<R>(FlatSource<SOA, R, T>{a}, Q, tl, true, 0u);
     // comparison_batch alone counts as comparison work but not as a fallback
     tl.flush<false>(a.stats);
 }
@@ -454,9 +476,136 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
         }
         push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
-        drain<SOA, R>(a, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+        drain<R>(FlatSource<SOA, R, T>{a}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
-    drain<SOA, R>(a, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    drain<R>(FlatSource<SOA, R, T>{a}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    tl.flush<true>(a.stats);
+}
+
+// ---- all-pairs particle-block kernel (BASELINE.json config 2) -----------------
+// One CTA per particle-pair block at a time (grid-stride over blocks): both
+// meshes are staged into shared memory in planar layout (coordinate c of
+// triangle t at m[c * tris + t], conflict-free for consecutive triangles),
+// then all tris x tris triangle pairs run the hybrid kernel from shared
+// memory -- the flat/multiscale callers' all-pairs meshgrid
+// (RK/stepping.py:285-308, RK/contact.py:97-140) without materialising the
+// pair list.  CONTACT pairs are compacted to a global list; every pair is
+// tallied in tc_stats.
+
+template <typename T>
+struct BlockArgs {
+    const T* meshes;          // [n_meshes][tris][9], world coordinates
+    int tris;
+    int64_t n_meshes;
+    const int32_t* blocks;    // [nb][2] mesh indices (A, B)
+    int64_t nb;
+    const T* block_eps;       // [nb] or NULL
+    T eps_scalar;
+    int64_t max_contacts;
+    int32_t* c_idx;           // [max][3] block, tri_a, tri_b
+    T* c_dist;                // [max]
+    T* c_pa;                  // [max][3]
+    T* c_pb;                  // [max][3]
+    unsigned long long* n_contacts;
+    tc_stats* stats;
+    double c_factor, alpha_it, alpha_reg, move_factor, start_coord;
+    int n_iterative;
+};
+
+template <class R, typename T>
+struct BlockSource {
+    const BlockArgs<T>& a;
+    const T* mA;
+    const T* mB;
+    int tris;
+    int64_t blk;
+    R eps;
+    __device__ __forceinline__ bool want_ids() const { return false; }
+    __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& e) const {
+        const int i = (int)(j / tris), k = (int)(j % tris);
+        A.p = mA + i;
+        A.stride = tris;
+        B.p = mB + k;
+        B.stride = tris;
+        e = eps;
+    }
+    __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const {
+        if (r.kind != KIND_CONTACT) return;
+        const unsigned long long slot = atomicAdd(a.n_contacts, 1ull);
+        if ((long long)slot >= a.max_contacts) return;  // counted, not stored
+        a.c_idx[3 * slot] = (int32_t)blk;
+        a.c_idx[3 * slot + 1] = (int32_t)(j / tris);
+        a.c_idx[3 * slot + 2] = (int32_t)(j % tris);
+        if (a.c_dist) a.c_dist[slot] = val(r.distance);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (a.c_pa) a.c_pa[3 * slot + c] = val(r.pa[c]);
+            if (a.c_pb) a.c_pb[3 * slot + c] = val(r.pb[c]);
+        }
+    }
+    __device__ __forceinline__ void store_ids01(int64_t, uint32_t) const {}
+};
+
+template <typename T, bool STRICT>
+__global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) blocks_hybrid_kernel(BlockArgs<T> a) {
+    using R = typename Pol<T, STRICT>::R;
+    __shared__ Queues Q;
+    extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
+    T* mA = reinterpret_cast<T*>(tc_dyn_smem) + 18 * BLOCK;  // after the crossing scratch
+    const int tris = a.tris;
+    T* mB = mA + 9 * tris;
+    const KP<R> kp = make_kp<R>(a);
+    Tally tl;
+    const int64_t P = (int64_t)tris * tris;
+    const int64_t ntile = (P + BLOCK - 1) / BLOCK;
+    for (int64_t blk = blockIdx.x; blk < a.nb; blk += gridDim.x) {
+        __syncthreads();  // the previous block is fully drained before its meshes are replaced
+        const int64_t ia = a.blocks[2 * blk], ib = a.blocks[2 * blk + 1];
+        const T* gA = a.meshes + ia * tris * 9;
+        const T* gB = a.meshes + ib * tris * 9;
+        for (int e = threadIdx.x; e < 9 * tris; e += BLOCK) {
+            const int t = e / 9, c = e - 9 * (e / 9);
+            mA[c * tris + t] = __ldg(gA + e);
+            mB[c * tris + t] = __ldg(gB + e);
+        }
+        if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
+        __syncthreads();
+        const R eps = R(a.block_eps ? a.block_eps[blk] : a.eps_scalar);
+        const BlockSource<R, T> src{a, mA, mB, tris, blk, eps};
+        for (int64_t tile = 0; tile < ntile; ++tile) {
+            const int64_t p = tile * BLOCK + threadIdx.x;
+            bool enq = false;
+            if (p < P) {
+                const int i = (int)(p / tris), k = (int)(p % tris);
+                const SmemTri<R> SA{mA + i, tris}, SB{mB + k, tris};
+                R A[9], B[9];
+#pragma unroll
+                for (int c = 0; c < 9; ++c) {
+                    A[c] = SA[c];
+                    B[c] = SB[c];
+                }
+                Rec<R> r;
+                run_iterative(SA, SB, A, B, eps, kp, r);
+                tl.iterative++;
+                if (r.kind == KIND_NOT_TERMINATED) {
+                    if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {
+                        r.kind = KIND_DEGENERATE;
+                        tl.degenerate++;
+                    } else {
+                        enq = true;
+                    }
+                }
+                if (!enq) {
+                    src.store(p, r);
+                    tl.result(r);
+                }
+            }
+            push(Q.q1, &Q.n1, enq, p);
+            __syncthreads();
+            drain<R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+        }
+        drain<R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    }
     tl.flush<true>(a.stats);
 }
 
@@ -591,6 +740,42 @@ static int run_device(int variant, const T* tri_a, const T* tri_b, int64_t n, co
     const bool strict = p->flags & TC_STRICT, soa = p->flags & TC_SOA;
     if (strict) return soa ? launch3<T, true, true>(variant, a, s) : launch3<T, true, false>(variant, a, s);
     return soa ? launch3<T, false, true>(variant, a, s) : launch3<T, false, false>(variant, a, s);
+}
+
+template <typename T>
+static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const int32_t* blocks, int64_t nb,
+                      const T* block_eps, const tc_params* p, int64_t max_contacts, int32_t* c_idx, T* c_dist,
+                      T* c_pa, T* c_pb, int64_t* n_contacts, tc_stats* stats, void* stream) {
+    if (!params_ok(p) || nb < 0 || tris < 1 || n_meshes < 1 || max_contacts < 0 || !n_contacts ||
+        (max_contacts > 0 && !c_idx) || (p->flags & (TC_SOA | TC_EMIT_IDS))) {
+        snprintf(g_err, sizeof(g_err), "invalid argument (blocks)");
+        return TC_EINVAL;
+    }
+    if (nb == 0) return TC_OK;
+    if (!meshes || !blocks) return TC_EINVAL;
+    const size_t smem = sizeof(T) * (18 * BLOCK + 18 * (size_t)tris);
+    if (smem > 200 * 1024) {
+        snprintf(g_err, sizeof(g_err), "tris_per_mesh %d too large for shared-memory staging", tris);
+        return TC_EINVAL;
+    }
+    BlockArgs<T> a;
+    a.meshes = meshes; a.tris = tris; a.n_meshes = n_meshes; a.blocks = blocks; a.nb = nb;
+    a.block_eps = block_eps; a.eps_scalar = (T)p->epsilon; a.max_contacts = max_contacts;
+    a.c_idx = c_idx; a.c_dist = c_dist; a.c_pa = c_pa; a.c_pb = c_pb;
+    a.n_contacts = reinterpret_cast<unsigned long long*>(n_contacts);
+    a.stats = stats;
+    a.c_factor = p->c_factor; a.alpha_it = p->alpha_iterative; a.alpha_reg = p->alpha_regulariser;
+    a.move_factor = p->move_factor; a.start_coord = p->start_coord; a.n_iterative = p->n_iterative;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto launch = [&](auto k) {
+        const int64_t g = grid_for(k, nb * (int64_t)BLOCK, smem);
+        k<<<(unsigned)(g < nb ? g : nb), BLOCK, smem, s>>>(a);
+    };
+    if (p->flags & TC_STRICT) launch(blocks_hybrid_kernel<T, true>);
+    else launch(blocks_hybrid_kernel<T, false>);
+    g_launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TC_OK : set_err("blocks launch", e);
 }
 
 // ---- host pipeline ----------------------------------------------------------------------
@@ -873,6 +1058,23 @@ int tc_degenerate_mask_host_f64(const double* tris, int64_t n, uint8_t* mask) {
 }
 int tc_degenerate_mask_host_f32(const float* tris, int64_t n, uint8_t* mask) {
     return tc::run_degenerate_host<float>(tris, n, mask);
+}
+
+int tc_blocks_hybrid_f64(const double* meshes, int32_t tris_per_mesh, int64_t n_meshes, const int32_t* blocks,
+                         int64_t n_blocks, const double* block_eps, const tc_params* p, int64_t max_contacts,
+                         int32_t* contact_idx, double* contact_distance, double* contact_point_a,
+                         double* contact_point_b, int64_t* n_contacts, tc_stats* stats, void* stream) {
+    return tc::run_blocks<double>(meshes, tris_per_mesh, n_meshes, blocks, n_blocks, block_eps, p, max_contacts,
+                                  contact_idx, contact_distance, contact_point_a, contact_point_b, n_contacts,
+                                  stats, stream);
+}
+int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_meshes, const int32_t* blocks,
+                         int64_t n_blocks, const float* block_eps, const tc_params* p, int64_t max_contacts,
+                         int32_t* contact_idx, float* contact_distance, float* contact_point_a,
+                         float* contact_point_b, int64_t* n_contacts, tc_stats* stats, void* stream) {
+    return tc::run_blocks<float>(meshes, tris_per_mesh, n_meshes, blocks, n_blocks, block_eps, p, max_contacts,
+                                 contact_idx, contact_distance, contact_point_a, contact_point_b, n_contacts, stats,
+                                 stream);
 }
 
 int tc_run_host_f64(int variant, const double* tri_a, const double* tri_b, int64_t n, const double* eps,

@@ -1,0 +1,98 @@
+"""All-pairs particle blocks (cfg2): tc_blocks_hybrid against the oracle
+(strict: bitwise) and against the flat hybrid kernel on the materialised
+pairs (fast: the same arithmetic, bitwise)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2105_12415_b200 import device as D  # noqa: E402
+from paper_2105_12415_b200 import particles as PT  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def scene():
+    meshes, blocks, gaps = PT.cfg2_scene(grid=(4, 4, 2))
+    return meshes, blocks, gaps
+
+
+def _contacts_from_flat(kind, dist, pa, pb, which, T):
+    rows = np.nonzero(kind == 1)[0]
+    blk = np.asarray(which)[rows // (T * T)]
+    i = (rows % (T * T)) // T
+    j = rows % T
+    idx = np.stack([blk, i, j], 1).astype(np.int32)
+    order = np.lexsort((idx[:, 2], idx[:, 1], idx[:, 0]))
+    return idx[order], dist[rows][order], pa[rows][order], pb[rows][order]
+
+
+@pytest.mark.parametrize("pkw", [dict(), dict(n_iterative=16, epsilon=1e-6), dict(epsilon=5e-2),
+                                 dict(n_iterative=16, epsilon=4e-2)])
+def test_blocks_strict_bitwise_vs_oracle(oracle_lib, scene, pkw):
+    meshes, blocks, gaps = scene
+    which = [int(np.argmin(gaps)), 0, 7]
+    T = meshes.shape[1]
+    st = D.new_stats()
+    out = PT.blocks_hybrid(torch.from_numpy(meshes).cuda(), torch.from_numpy(blocks[which]).cuda(),
+                           D.Params(**pkw), strict=True, stats=st)
+    torch.cuda.synchronize()
+    got = PT.sort_contacts(out)
+    # block ids in the device result are positions in `which`
+    A, B = PT.block_pairs(meshes, blocks, which)
+    p = oracle_lib.make_params(**pkw)
+    ref, counts, rc = oracle_lib.hybrid(A, B, p, p.epsilon, threads=oracle_lib.default_threads())
+    assert rc == 0
+    idx, dist, pa, pb = _contacts_from_flat(ref["kind"], ref["distance"], ref["point_a"], ref["point_b"],
+                                            range(len(which)), T)
+    assert got["n_contacts"] == len(idx)
+    if pkw.get("epsilon", 1e-2) >= 4e-2:
+        assert len(idx) > 0   # the facets of icosphere(2) sit ~0.07 apart at the closest blocks
+    assert np.array_equal(got["idx"], idx)
+    assert np.array_equal(got["distance"], dist)
+    assert np.array_equal(got["point_a"], pa) and np.array_equal(got["point_b"], pb)
+    s = D.read_stats(st)
+    assert [s["iterative"], s["comparison"], s["fallback"]] == list(counts[:3])
+    assert s["contacts"] == len(idx)
+    assert s["min_distance"] == float(ref["distance"].min())
+
+
+def test_blocks_fast_equals_flat_fast(scene):
+    meshes, blocks, gaps = scene
+    which = [int(b) for b in np.argsort(gaps)[:12]]
+    T = meshes.shape[1]
+    pk = dict(epsilon=5e-2)
+    st = D.new_stats()
+    out = PT.blocks_hybrid(torch.from_numpy(meshes).cuda(), torch.from_numpy(blocks[which]).cuda(),
+                           D.Params(**pk), strict=False, stats=st)
+    A, B = PT.block_pairs(meshes, blocks, which)
+    st2 = D.new_stats()
+    flat = D.run("hybrid", torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), D.Params(**pk), stats=st2)
+    torch.cuda.synchronize()
+    got = PT.sort_contacts(out)
+    idx, dist, pa, pb = _contacts_from_flat(flat["kind"].cpu().numpy(), flat["distance"].cpu().numpy(),
+                                            flat["point_a"].cpu().numpy(), flat["point_b"].cpu().numpy(),
+                                            range(len(which)), T)
+    assert got["n_contacts"] == len(idx) > 0
+    assert np.array_equal(got["idx"], idx) and np.array_equal(got["distance"], dist)
+    s1, s2 = D.read_stats(st), D.read_stats(st2)
+    for k in ("iterative", "comparison", "fallback", "contacts", "intersecting", "min_distance"):
+        assert s1[k] == s2[k], k
+
+
+def test_blocks_contact_capacity_and_empty(scene):
+    meshes, blocks, gaps = scene
+    which = np.argsort(gaps)[:4]
+    out = PT.blocks_hybrid(torch.from_numpy(meshes).cuda(), torch.from_numpy(blocks[which]).cuda(),
+                           D.Params(epsilon=6e-2), max_contacts=3)
+    torch.cuda.synchronize()
+    n = int(out["n_contacts"].item())
+    assert n > 3                                       # all counted ...
+    res = PT.sort_contacts(out)
+    assert res["idx"].shape == (3, 3)                  # ... only max_contacts stored
+    empty = PT.blocks_hybrid(torch.from_numpy(meshes).cuda(), torch.zeros((0, 2), dtype=torch.int32).cuda(),
+                             D.Params())
+    assert int(empty["n_contacts"].item()) == 0
