@@ -52,7 +52,7 @@ static inline REAL FN(max_)(REAL a, REAL b) { return (a >= b) ? a : b; }
 /* Decision margins of the last helper call on this thread (test-side tie
  * classification of the FMA build, tests/parity.py); they do not feed back
  * into any result. */
-static __thread double FN(tl_pt_d_), FN(tl_pt_v_), FN(tl_seg_), FN(tl_cx_plane_), FN(tl_cx_inside_);
+static __thread double FN(tl_pt_d_), FN(tl_pt_v_), FN(tl_seg_), FN(tl_cx_plane_), FN(tl_cx_inside_), FN(tl_cx_cond_);
 
 static inline double FN(fabsd_)(double x) { return x < 0 ? -x : x; }
 static inline double FN(mind_)(double a, double b) { return a < b ? a : b; }
@@ -253,6 +253,8 @@ static int FN(segment_triangle_crossing_)(const REAL* p, const REAL* q, const RE
     {
         double nn = sqrt((double)nrm[0] * nrm[0] + (double)nrm[1] * nrm[1] + (double)nrm[2] * nrm[2]);
         FN(tl_cx_plane_) = nn > 0 ? FN(mind_)(FN(fabsd_)(dp), FN(fabsd_)(dq)) / nn : 0;
+        /* conditioning of the 2x2 barycentric solve: (uu + vv)^2 / |det| */
+        FN(tl_cx_cond_) = FN(fabsd_)(det) > 0 ? ((double)uu + vv) * ((double)uu + vv) / FN(fabsd_)(det) : 1e300;
         FN(tl_cx_inside_) = crossing ? FN(mind_)(FN(mind_)(FN(fabsd_)(b1), FN(fabsd_)(b2)),
                                                  FN(fabsd_)(1.0 - (double)b1 - b2)) : 1e300;
     }
@@ -351,12 +353,14 @@ static void FN(comparison_one_)(const REAL* A, const REAL* B, REAL eps, FN(rec_)
     /* six edge-to-plane tests */
     REAL pts[6][3];
     int ok[6], any = 0;
-    double cx_plane = 1e300, cx_inside = 1e300;
+    double cx_plane = 1e300, cx_inside = 1e300, cx_cond = 0;
     for (int k = 0; k < 3; ++k) {
         ok[k] = FN(segment_triangle_crossing_)(A + 3 * FN(EDGE_START_)[k], A + 3 * FN(EDGE_END_)[k], B, pts[k]);
         cx_plane = FN(mind_)(cx_plane, FN(tl_cx_plane_)); cx_inside = FN(mind_)(cx_inside, FN(tl_cx_inside_));
+        cx_cond = cx_cond > FN(tl_cx_cond_) ? cx_cond : FN(tl_cx_cond_);
         ok[k + 3] = FN(segment_triangle_crossing_)(B + 3 * FN(EDGE_START_)[k], B + 3 * FN(EDGE_END_)[k], A, pts[k + 3]);
         cx_plane = FN(mind_)(cx_plane, FN(tl_cx_plane_)); cx_inside = FN(mind_)(cx_inside, FN(tl_cx_inside_));
+        cx_cond = cx_cond > FN(tl_cx_cond_) ? cx_cond : FN(tl_cx_cond_);
         any |= ok[k] | ok[k + 3];
     }
     uint8_t pair_id = 255;
@@ -403,7 +407,7 @@ static void FN(comparison_one_)(const REAL* A, const REAL* B, REAL eps, FN(rec_)
     out->mg[3] = cx_inside;
     out->mg[7] = win_margin;
     out->mg[8] = (double)SQRT(best);
-    out->mg[9] = 0;
+    out->mg[9] = cx_cond;
 }
 
 /* RK/kernels.py:417-431 _penalty_value, summed left to right. */
@@ -709,7 +713,8 @@ int FN(tco_hybrid_)(const REAL* A, const REAL* B, int64_t n, const REAL* eps,
  * whose endpoints straddle the plane, [4] |dJ| - c eps, [5] move - mf eps,
  * [6] J_hat - 2 eps^2, [7] normalised region / segment-branch margin of the
  * winning feature, [8] the feature distance before the crossing override
- * (the answer had no crossing been found), [9] reserved.  Test-side tie
+ * (the answer had no crossing been found), [9] max conditioning
+ * (uu + vv)^2 / |det| of the six barycentric solves.  Test-side tie
  * classification only. */
 int FN(tco_margins_)(const REAL* A, const REAL* B, int64_t n, const REAL* eps, const tco_params* p,
                      double* margins, int threads) {

@@ -199,16 +199,13 @@ def touching(rng, m):
     B[:, 0] = A[:, 0] + a[:, None] * e1 + b[:, None] * e2
     scale = 1.0 / np.maximum(np.abs(nrm).max(axis=1), 1.0)
     scale = 2.0 ** np.floor(np.log2(scale))[:, None]  # dyadic
-    for k in (1, 2):
-        inplane = rng.integers(-8, 9, (m, 3)) / 32.0
-        off = inplane - (np.einsum("ij,ij->i", inplane, nrm) / np.einsum("ij,ij->i", nrm, nrm))[:, None] * nrm
-        off = np.round(off * 32.0) / 32.0
+    # B's other vertices: a lift along A's normal plus an in-plane step along
+    # A's edge e1 (for v1) or e2 (for v2) -- independent directions, so B is
+    # never degenerate, and exactly in the closed positive half-space
+    for k, e in ((1, e1), (2, e2)):
+        step = rng.integers(1, 5, m)[:, None] / 16.0 * rng.choice([-1.0, 1.0], (m, 1))
         lift = rng.integers(1, 9, m)[:, None] * scale * nrm * 4.0
-        cand = B[:, 0] + off + lift
-        # enforce the half-space: keep only offsets with non-negative normal part
-        neg = np.einsum("ij,ij->i", cand - A[:, 0], nrm) < 0
-        cand[neg] = B[neg, 0] + lift[neg]
-        B[:, k] = cand
+        B[:, k] = B[:, 0] + step * e + lift
     return A, B
 
 

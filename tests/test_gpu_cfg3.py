@@ -1,0 +1,67 @@
+"""Adversarial robustness set (BASELINE.json config 3): near-parallel faces,
+edge-edge crossings, slivers (aspect 1e4-1e5), exactly touching dyadic
+vertex-face pairs.  Strict: bitwise vs the oracle; fast: the tie-aware
+tolerance check, per class."""
+
+import numpy as np
+import pytest
+
+from conftest import PARAM_SETS
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2105_12415_b200 import device as D  # noqa: E402
+from paper_2105_12415_b200 import workloads as W  # noqa: E402
+
+import parity  # noqa: E402
+
+N_PER = 1 << 15
+
+
+@pytest.fixture(scope="module")
+def cfg3():
+    return W.adversarial_pairs(N_PER, seed=3)
+
+
+def _run(A, B, pkw, strict, dt):
+    t = {np.float64: torch.float64, np.float32: torch.float32}[dt]
+    out = D.run("hybrid", torch.from_numpy(A.astype(dt)).cuda(), torch.from_numpy(B.astype(dt)).cuda(),
+                D.Params(**pkw), strict=strict, ids=True)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+@pytest.mark.parametrize("pname", list(PARAM_SETS))
+def test_cfg3_strict_bitwise(oracle_lib, cfg3, pname):
+    A, B = cfg3
+    pkw = PARAM_SETS[pname]
+    got = _run(A, B, pkw, True, np.float64)
+    p = oracle_lib.make_params(**pkw)
+    ref, _, rc = oracle_lib.hybrid(A, B, p, p.epsilon, threads=oracle_lib.default_threads())
+    for k in ("kind", "distance", "point_a", "point_b", "bary_a", "bary_b", "ids"):
+        assert np.array_equal(got[k], ref[k]), k
+    fb = (ref["ids"][:, 3] & 4) > 0
+    rates = fb.reshape(4, N_PER).mean(axis=1)
+    print(f"cfg3 {pname}: fallback rate per class {dict(zip(W.CFG3_CLASSES, np.round(rates, 4)))}")
+    # touching class: the exact (comparison) distance is 0 for every pair
+    cm = oracle_lib.comparison(A[3 * N_PER:], B[3 * N_PER:], p.epsilon, threads=oracle_lib.default_threads())
+    assert np.all(cm["distance"] == 0.0)
+
+
+@pytest.mark.parametrize("real", ["float64", "float32"])
+def test_cfg3_fast_within_tolerance(oracle_lib, cfg3, real):
+    dt = np.float64 if real == "float64" else np.float32
+    A, B = cfg3
+    pkw = PARAM_SETS["bl"]
+    got = _run(A, B, pkw, False, dt)
+    for c, name in enumerate(W.CFG3_CLASSES):
+        sl = slice(c * N_PER, (c + 1) * N_PER)
+        sub = {k: v[sl] for k, v in got.items()}
+        # adversarial classes are built around ties (exact touching, crossings
+        # through a vertex, near-parallel faces): a larger share of excused ties
+        rep = parity.compare_fast(oracle_lib, "hybrid", A[sl].astype(dt), B[sl].astype(dt), pkw, sub, dt,
+                                  max_excused=0.02 if dt == np.float64 else 0.06)
+        assert rep["ok"], f"{name}: {rep}"

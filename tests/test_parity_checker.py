@@ -36,7 +36,7 @@ def test_fma_build_within_tolerance(oracle_lib, fma, golden_inputs, variant, cas
     B = golden_inputs[f"{case}_B"].astype(dt)
     got = _run(fma, variant, A, B, PARAM_SETS[pname], dt)
     rep = parity.compare_fast(oracle_lib, variant, A, B, PARAM_SETS[pname], got, dt)
-    assert rep["ok"], rep
+    assert rep["ok"], str(rep)
 
 
 def test_strict_oracle_against_itself_is_exact(oracle_lib, golden_inputs):
