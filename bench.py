@@ -43,6 +43,8 @@ import numpy as np  # noqa: E402
 N_PAIRS = 1 << 24
 PARAMS = dict(n_iterative=16, epsilon=1e-6)
 SEP = (-0.1, 0.5)
+CFG4_PAIRS = 1 << 28
+CFG4_SEP = (-0.05, 0.2)
 METRIC = "triangle-pair contact queries/sec (hybrid, fp64)"
 UNIT = "pairs/s"
 
@@ -177,6 +179,9 @@ def main():
     ap.add_argument("--n", type=int, default=N_PAIRS, help="pairs per GPU")
     ap.add_argument("--strict", action="store_true", help="time the bit-exact TC_STRICT build")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu baseline / variant table")
+    ap.add_argument("--config", default="cfg1", choices=["cfg1", "cfg4"],
+                    help="cfg1: 2^24 pairs per GPU, full record (weak scaling, default); "
+                         "cfg4: 2^28 pairs in total sharded over the GPUs, reduce-only (strong scaling)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -195,13 +200,31 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     lib = _abi.load()
-    n = args.n
+    cfg4 = args.config == "cfg4"
+    if cfg4:
+        n_total = args.n if args.n != N_PAIRS else CFG4_PAIRS
+        start, n = shard.shard_range(n_total, rank, world)
+        sep = CFG4_SEP
+    else:
+        n, start, sep = args.n, rank * args.n, SEP
 
-    # ---- inputs: this rank's range of the cfg1 generator, SoA planes in HBM
-    A, B = W.random_pairs(n, seed=0, sep=SEP, start=rank * n)
-    planes = torch.from_numpy(W.to_soa(A, B)).to(dev)
+    # ---- inputs: this rank's range of the chunked generator, SoA planes in HBM
+    # (generated on all host cores in slices, uploaded slice by slice)
+    planes = torch.empty((18, n), dtype=torch.float64, device=dev)
+    A = B = None
+    slice_n = 1 << 23
+    for lo in range(0, n, slice_n):
+        hi = min(n, lo + slice_n)
+        a, b = W.random_pairs_mp(hi - lo, seed=0, sep=sep, start=start + lo)
+        planes[:, lo:hi] = torch.from_numpy(W.to_soa(a, b)).to(dev)
+        if not cfg4:
+            if A is None:
+                A = np.empty((n, 3, 3))
+                B = np.empty((n, 3, 3))
+            A[lo:hi] = a
+            B[lo:hi] = b
     ta, tb = planes[:9], planes[9:]
-    out = D.alloc_outputs(n, torch.float64, dev, soa=True)
+    out = {} if cfg4 else D.alloc_outputs(n, torch.float64, dev, soa=True)
     stats = D.new_stats(dev)
     params = D.Params(**PARAMS)
     stream = torch.cuda.current_stream(dev)
@@ -244,12 +267,13 @@ def main():
     ms_total, ms_kernel = float(t[0]), float(t[1])
     ms_step = ms_total / args.steps
     st = shard.stats_dict(stats)  # after the last step's all-reduce: whole-job tallies
-    value = n * world / (ms_step / 1e3)
+    n_job = n_total if cfg4 else n * world
+    value = n_job / (ms_step / 1e3)
 
     # ---- roofline of the dominant kernel (hybrid_kernel): FP64 pipe
     n_local = n
-    fb_local = st["fallback"] / world
-    fbx_local = st["intersecting"] / world
+    fb_local = st["fallback"] * n_local / n_job
+    fbx_local = st["intersecting"] * n_local / n_job
     flops = flops_executed(n_local, PARAMS["n_iterative"], fb_local, fbx_local)
     flops_ref = flops_reference_model(n_local, PARAMS["n_iterative"], fb_local, fbx_local)
     achieved_tf = flops / (ms_kernel / 1e3) / 1e12
@@ -265,7 +289,7 @@ def main():
         torch.cuda.synchronize()
         best = max(best, fl / (e0.elapsed_time(e1) / 1e3) / 1e12)
     peak_tf = best
-    bytes_per_pair = 144 + 89  # SoA inputs + full result record
+    bytes_per_pair = 144 if cfg4 else 144 + 89  # SoA inputs (+ full result record unless reduce-only)
     hbm_gbs = n_local * bytes_per_pair / (ms_kernel / 1e3) / 1e9
     peaks = {}
     try:
@@ -279,7 +303,7 @@ def main():
     if prof.exists():
         try:
             pj = json.loads(prof.read_text())
-            if pj.get("n") == n_local:
+            if pj.get("n") == n_local and not cfg4:
                 traffic = pj.get("dram_bytes_per_launch")
                 traffic_note = pj.get("source")
         except ValueError:
@@ -287,7 +311,7 @@ def main():
     roofline = {
         "bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
         "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
-        "traffic_source": traffic_note, "algorithmic_bytes_per_launch": n_local * 233,
+        "traffic_source": traffic_note, "algorithmic_bytes_per_launch": n_local * bytes_per_pair,
         "kernel": "hybrid_kernel<double,fast,soa>", "kernel_ms": ms_kernel,
         "flops_per_launch": flops,
         "flop_model": "executed: n(200+88N) + 1199 (fallback - fallback&intersect) + 522 fallback&intersect "
@@ -298,24 +322,34 @@ def main():
                 "bytes_per_pair": bytes_per_pair, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
     }
 
+    if cfg4:
+        cfg = {"workload": "cfg4: 2^28 random triangle pairs in total, sep U[-0.05,0.2], hybrid fp64, 16 sweeps, "
+                           "eps 1e-6, reduce-only (tc_stats), contiguous shards",
+               "pairs_total": n_total, "pairs_per_gpu": n, "layout": "SoA [18][n] in HBM",
+               "rounding": "strict" if args.strict else "fast",
+               "l2": f"inputs {n * 144 / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
+               "parallelism": f"dp{world} contiguous shards + NCCL all-reduce of stats" if world > 1 else "1 GPU"}
+    else:
+        cfg = {"workload": "cfg1: 2^24 random triangle pairs per GPU, hybrid fp64, 16 sweeps, eps 1e-6",
+               "pairs_per_gpu": n, "layout": "SoA [18][n] in HBM", "rounding": "strict" if args.strict else "fast",
+               "l2": "inputs 2.4 GB + outputs 1.5 GB per GPU > 126 MB L2 (no flush needed)",
+               "parallelism": f"dp{world} contiguous shards + NCCL all-reduce of stats" if world > 1 else "1 GPU"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if cfg4 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg0/cfg1 generator, SURVEY.md 8d)",
-        "config": {"workload": "cfg1: 2^24 random triangle pairs per GPU, hybrid fp64, 16 sweeps, eps 1e-6",
-                   "pairs_per_gpu": n, "layout": "SoA [18][n] in HBM", "rounding": "strict" if args.strict else "fast",
-                   "l2": "inputs 2.4 GB + outputs 1.5 GB per GPU > 126 MB L2 (no flush needed)",
-                   "parallelism": f"dp{world} contiguous shards + NCCL all-reduce of stats" if world > 1 else "1 GPU"},
+        "config": cfg,
         "roofline": roofline,
         "gpu_launches": launches,
         "stats": st,
-        "fallback_rate": st["fallback"] / (n * world),
+        "fallback_rate": st["fallback"] / n_job,
     }
 
     clocks = clk.summary()
     line["clocks"] = clocks
 
-    if not args.no_extras:
+    if not args.no_extras and not cfg4:
         # ---- e2e through the host C-ABI entry point (pinned host buffers)
         line["e2e"] = e2e_measure(lib, _abi, torch, A, B, n, world, dist, dev)
         if rank == 0 and world == 1:
@@ -325,6 +359,7 @@ def main():
                                     "sample": f"{done} pairs of the cfg1 generator in 131072-pair chunks, hybrid "
                                               "(16, 1e-6), oracle/tc_oracle.c on all host threads"}
             line["variants"] = variant_table(D, torch, A[: 1 << 22], B[: 1 << 22], dev)
+            line["configs"] = configs_table(D, torch, dev)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -367,6 +402,55 @@ def e2e_measure(lib, _abi, torch, A, B, n, world, dist, dev, reps=3):
     return {"value": n * world / sec, "unit": UNIT, "h2d_bytes_per_step": n * 144 * world,
             "d2h_bytes_per_step": n * 89 * world, "ms_per_step": 1e3 * sec,
             "path": "tc_run_host_f64 (host C ABI, pinned, 1M-pair chunks on 3 streams)"}
+
+
+def configs_table(D, torch, dev):
+    """The other BASELINE.json configs on this GPU: cfg2 (all-pairs particle
+    blocks, full 2,048-particle scene) and cfg3 (adversarial set, per class)."""
+    from paper_2105_12415_b200 import particles as PT, workloads as W
+    res = {}
+    meshes, blocks, gaps = PT.cfg2_scene()
+    tm = torch.from_numpy(meshes).to(dev)
+    tb = torch.from_numpy(blocks).to(dev)
+    P = D.Params(**PARAMS)
+    n_pairs = int(blocks.shape[0]) * meshes.shape[1] ** 2
+    for strict in (False, True):
+        st = D.new_stats(dev)
+        PT.blocks_hybrid(tm, tb, P, strict=strict, stats=st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        D.reset_stats(st)
+        e0.record()
+        out = PT.blocks_hybrid(tm, tb, P, strict=strict, stats=st)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        s = D.read_stats(st)
+        res[f"cfg2_{'strict' if strict else 'fast'}"] = {
+            "pairs": n_pairs, "blocks": int(blocks.shape[0]), "ms": ms, "pairs_per_s": n_pairs / (ms / 1e3),
+            "fallback_rate": s["fallback"] / n_pairs, "contacts": int(out["n_contacts"].item()),
+            "min_distance": s["min_distance"]}
+    # cfg3: 2^20 pairs per class, hybrid (16, 1e-6)
+    A, B = W.adversarial_pairs(1 << 20, seed=3)
+    c3 = {}
+    for c, name in enumerate(W.CFG3_CLASSES):
+        sl = slice(c << 20, (c + 1) << 20)
+        planes = torch.from_numpy(W.to_soa(A[sl], B[sl])).to(dev)
+        st = D.new_stats(dev)
+        D.run("hybrid", planes[:9], planes[9:], P, soa=True, out={}, n=1 << 20)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        D.run("hybrid", planes[:9], planes[9:], P, soa=True, stats=st, n=1 << 20)
+        e1.record()
+        torch.cuda.synchronize()
+        s = D.read_stats(st)
+        c3[name] = {"pairs": 1 << 20, "pairs_per_s": (1 << 20) / (e0.elapsed_time(e1) / 1e3),
+                    "fallback_rate": s["fallback"] / (1 << 20), "degenerate": s["degenerate"],
+                    "contacts": s["contacts"]}
+    res["cfg3_fast"] = c3
+    res["note"] = ("oracle agreement of cfg2/cfg3: tests/test_gpu_blocks.py, tests/test_gpu_cfg3.py "
+                   "(strict bitwise, fast within tolerance with the tie classifier)")
+    return res
 
 
 def variant_table(D, torch, A, B, dev, reps=3):

@@ -98,6 +98,47 @@ def random_pairs(n: int, seed: int = 0, sep=(-0.1, 0.5), start: int = 0,
     return A, B
 
 
+def _mp_worker(args):
+    name, shape, dtype, seed, sep, start, lo, hi = args
+    from multiprocessing import shared_memory
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        buf = np.ndarray(shape, dtype=dtype, buffer=shm.buf)
+        A, B = random_pairs(hi - lo, seed=seed, sep=sep, start=start + lo, dtype=dtype, threads=1)
+        buf[0, lo:hi] = A
+        buf[1, lo:hi] = B
+    finally:
+        shm.close()
+
+
+def random_pairs_mp(n: int, seed: int = 0, sep=(-0.1, 0.5), start: int = 0, dtype=np.float64,
+                    processes: int | None = None):
+    """random_pairs for large n on all host cores (process pool + shared memory);
+    bit-identical to random_pairs (same per-chunk streams)."""
+    import multiprocessing as mp
+    import os
+    from multiprocessing import shared_memory
+    processes = processes or len(os.sched_getaffinity(0))
+    if processes <= 1 or n < 64 * CHUNK:
+        return random_pairs(n, seed=seed, sep=sep, start=start, dtype=dtype)
+    shape = (2, n, 3, 3)
+    shm = shared_memory.SharedMemory(create=True, size=int(np.prod(shape)) * np.dtype(dtype).itemsize)
+    try:
+        # split on chunk boundaries of the absolute index so every chunk is generated once
+        edges = sorted({0, n} | {min(n, max(0, k * CHUNK - start)) for k in
+                                 range(start // CHUNK, (start + n) // CHUNK + 1, max(1, (n // CHUNK) // (4 * processes)))})
+        jobs = [(shm.name, shape, np.dtype(dtype).str, seed, sep, start, lo, hi) for lo, hi in zip(edges, edges[1:]) if hi > lo]
+        with mp.get_context("fork").Pool(processes) as pool:
+            pool.map(_mp_worker, jobs)
+        buf = np.ndarray(shape, dtype=dtype, buffer=shm.buf)
+        A = buf[0].copy()
+        B = buf[1].copy()
+    finally:
+        shm.close()
+        shm.unlink()
+    return A, B
+
+
 def to_soa(A: np.ndarray, B: np.ndarray) -> np.ndarray:
     """(n,3,3) x 2 -> planar [18][n]: planes 0-8 are A's v0x..v2z, 9-17 B's."""
     n = A.shape[0]
