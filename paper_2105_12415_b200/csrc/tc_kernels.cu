@@ -110,11 +110,11 @@ __device__ __forceinline__ void stash_pair(T* slot, const R* A, const R* B) {
 // Iterative kernel for one pair: the reference's operation order in strict
 // mode, the Gram-matrix form in the fast build (tc_pair.cuh).  SA / SB give
 // the epilogue's re-reads of the pair (a shared-memory copy).
-template <class R, class TA, class TB>
-__device__ __forceinline__ void run_iterative(const TA& SA, const TB& SB, const R* A, const R* B, R eps,
+template <class R, class TA, class TB, class EpsFn>
+__device__ __forceinline__ void run_iterative(const TA& SA, const TB& SB, const R* A, const R* B, EpsFn eps_fn,
                                               const KP<R>& kp, Rec<R>& r) {
     if constexpr (IsStrict<R>::value) {
-        iterative_pair(A, B, eps, kp, r, [&](R* A0, R* B0) {
+        iterative_pair(A, B, eps_fn(), kp, r, [&](R* A0, R* B0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 A0[k] = SA[k];
@@ -122,7 +122,7 @@ __device__ __forceinline__ void run_iterative(const TA& SA, const TB& SB, const 
             }
         });
     } else {
-        auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4) {
+        auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4, R* sq, R* eps_out) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 const R a0 = SA[k], b0 = SB[k];
@@ -133,15 +133,22 @@ __device__ __forceinline__ void run_iterative(const TA& SA, const TB& SB, const 
                 E3[k] = b0 - SB[3 + k];
                 E4[k] = b0 - SB[6 + k];
             }
+            if (sq) {
+                R ta[9], tb[9];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) { ta[k] = SA[k]; tb[k] = SB[k]; }
+                *sq = maxv(max_sq_edge(ta), max_sq_edge(tb));
+                *eps_out = eps_fn();
+            }
         };
-        if (kp.start_coord >= R(0) && kp.start_coord <= R(1)) iterative_pair_gram<true>(A, B, eps, kp, r, reload);
-        else iterative_pair_gram<false>(A, B, eps, kp, r, reload);
+        if (kp.start_coord >= R(0) && kp.start_coord <= R(1)) iterative_pair_gram<true>(A, B, kp, r, reload);
+        else iterative_pair_gram<false>(A, B, kp, r, reload);
     }
 }
-template <class R, typename T>
-__device__ __forceinline__ void run_iterative(const T* slot, const R* A, const R* B, R eps, const KP<R>& kp,
+template <class R, typename T, class EpsFn>
+__device__ __forceinline__ void run_iterative(const T* slot, const R* A, const R* B, EpsFn eps_fn, const KP<R>& kp,
                                               Rec<R>& r) {
-    run_iterative(SmemTri<R>{slot, BLOCK}, SmemTri<R>{slot + 9 * BLOCK, BLOCK}, A, B, eps, kp, r);
+    run_iterative(SmemTri<R>{slot, BLOCK}, SmemTri<R>{slot + 9 * BLOCK, BLOCK}, A, B, eps_fn, kp, r);
 }
 
 template <bool SOA, class R, typename T>
@@ -423,7 +430,7 @@ __global__ void __launch_bounds__(BLOCK, TC_ITER_MINB) iterative_kernel(Args<T> 
         T* slot = thread_slot<T>(0);
         stash_pair(slot, A, B);
         Rec<R> r;
-        run_iterative(slot, A, B, eps, kp, r);
+        run_iterative(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
         store_rec<SOA>(a, i, r);
         tl.iterative++;
         tl.result(r);
@@ -457,7 +464,7 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
             T* slot = thread_slot<T>(18 * BLOCK);  // the comparison phases' pair slot, free here
             stash_pair(slot, A, B);
             Rec<R> r;
-            run_iterative(slot, A, B, eps, kp, r);
+            run_iterative(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
             tl.iterative++;
             if (r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i])) {
                 const SmemTri<R> SA{slot, BLOCK}, SB{slot + 9 * BLOCK, BLOCK};
@@ -585,7 +592,7 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) blocks_hybrid_kernel(Bl
                     B[c] = SB[c];
                 }
                 Rec<R> r;
-                run_iterative(SA, SB, A, B, eps, kp, r);
+                run_iterative(SA, SB, A, B, [&] { return eps; }, kp, r);
                 tl.iterative++;
                 if (r.kind == KIND_NOT_TERMINATED) {
                     if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {

@@ -716,13 +716,13 @@ __device__ __forceinline__ void iterative_pair(const R* A, const R* B, R eps, co
 // is rebuilt exactly from x where the settle test needs it.  Equal to the
 // reference up to rounding (checked within the north-star tolerance).
 template <bool BOX, class R, class Reload>
-__device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R eps, const KP<R>& kp, Rec<R>& o,
+__device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, const KP<R>& kp, Rec<R>& o,
                                                     Reload reload) {
     using T = typename Store<R>::type;
     const R tiny = R(Tiny<R>::v);
     const R half = R(T(0.5));
     R G00, G01, G03, G04, G11, G13, G14, G33, G34, G44, SA0, SA1, SA3, SA4, SB0, SB1, SB3, SB4;
-    R r0, r1, r2, r3, r3a, r3b, alpha_it;
+    R r0, r1, r2, r3, r3a, r3b;
     R x0 = kp.start_coord, x1 = kp.start_coord, x2 = kp.start_coord, x3 = kp.start_coord;
     R g0, g1, g3, g4;
     {
@@ -742,7 +742,6 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R ep
         SA0 = dot3(SA, E0); SA1 = dot3(SA, E1); SA3 = dot3(SA, E3); SA4 = dot3(SA, E4);
         SB0 = dot3(SB, E0); SB1 = dot3(SB, E1); SB3 = dot3(SB, E3); SB4 = dot3(SB, E4);
         const R sq = maxv(max_sq_edge(A), max_sq_edge(B));
-        alpha_it = kp.alpha_it * sq;
         const R alpha_reg = kp.alpha_reg * sq;
         r0 = rcpv(maxv(G00 + alpha_reg, tiny));
         r1 = rcpv(maxv(G11 + alpha_reg, tiny));
@@ -792,16 +791,20 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, R ep
 #pragma unroll
         for (int i = 0; i < 3; ++i) d[i] = (A0[i] - B0[i]) + x0 * E0[i] + x1 * E1[i] + x2 * E3[i] + x3 * E4[i];
     };
-    R j_old, mid_old[3];
+    // the penalty weight and the halo are re-derived here rather than kept
+    // live through the sweep loop (register pressure)
+    R j_old, mid_old[3], alpha_it, eps;
     {
-        reload(A0, B0, E0, E1, E3, E4);
+        R sq;
+        reload(A0, B0, E0, E1, E3, E4, &sq, &eps);
+        alpha_it = kp.alpha_it * sq;
         diff();
         R xs[4] = {x0, x1, x2, x3};
         j_old = half * dot3(d, d) + penalty(xs, alpha_it);
         contact_mid(A0, xs, E0, E1, d, mid_old);
     }
     sweep();
-    reload(A0, B0, E0, E1, E3, E4);
+    reload(A0, B0, E0, E1, E3, E4, nullptr, nullptr);
     diff();
     R xs[4] = {x0, x1, x2, x3};
     const R dd = dot3(d, d);
