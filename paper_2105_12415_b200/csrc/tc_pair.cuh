@@ -535,6 +535,8 @@ __device__ __forceinline__ void contact_mid(const R* A0, const R* x, const R* e1
 // clip0_hi(x, hi) == np.clip(x, 0, hi) bit for bit for hi >= +0 (x <= 0,
 // including -0, gives +0; ties give hi), so strict mode uses it too.
 __device__ __forceinline__ double negv(double x) {
+    // (ptxas turns this into a DADD; forcing an integer xor through PTX
+    // measured slower: the extra register moves cost more than the DADD)
     return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
 }
 __device__ __forceinline__ float negv(float x) { return __int_as_float(__float_as_int(x) ^ (int)0x80000000); }
@@ -757,24 +759,64 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, cons
     // the box, so the inner max() of the clips are identities (coord_step)
     auto hi_of = [&](R xp) { return BOX ? R(1) - xp : maxv(R(0), R(1) - maxv(xp, R(0))); };
     auto clip_lo0 = [&](R v, R hi) { return clip0_hi(v, hi); };
+#ifndef TC_HTRICK
+#define TC_HTRICK 0
+#endif
     auto sweep = [&]() {
         R t, s;
+#if TC_HTRICK
+        // the gradient the next substep reads is formed as t*G + (g - x*G),
+        // the bracket computed while the clip is still pending: the step's
+        // DADD leaves the dependent chain (one extra FMA per critical g)
+        {
+            const R h1 = g1 - x0 * G01;
+            t = clip_lo0(x0 - g0 * r0, hi_of(x1));
+            s = t - x0; x0 = t;
+            g1 = h1 + t * G01;
+            g0 += s * G00; g3 += s * G03; g4 += s * G04;
+        }
+        {
+            const R h0 = g0 - x1 * G01, h1 = g1 - x1 * G11;
+            t = clip_lo0(x1 - g1 * r1, hi_of(x0));
+            s = t - x1; x1 = t;
+            g0 = h0 + t * G01; g1 = h1 + t * G11;
+            g3 += s * G13; g4 += s * G14;
+        }
+#else
         t = clip_lo0(x0 - g0 * r0, hi_of(x1));
         s = t - x0; x0 = t;
         g0 += s * G00; g1 += s * G01; g3 += s * G03; g4 += s * G04;
         t = clip_lo0(x1 - g1 * r1, hi_of(x0));
         s = t - x1; x1 = t;
         g0 += s * G01; g1 += s * G11; g3 += s * G13; g4 += s * G14;
+#endif
         t = -(g1 - g0) * r3a;
         t = BOX ? clip_sym(t, x1, x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
         x0 = x0 - t; x1 = x1 + t;
         g0 += t * SA0; g1 += t * SA1; g3 += t * SA3; g4 += t * SA4;
+#if TC_HTRICK
+        {
+            const R h4 = g4 - x2 * G34;
+            t = clip_lo0(x2 - g3 * r2, hi_of(x3));
+            s = t - x2; x2 = t;
+            g4 = h4 + t * G34;
+            g0 += s * G03; g1 += s * G13; g3 += s * G33;
+        }
+        {
+            const R h3 = g3 - x3 * G34, h4 = g4 - x3 * G44;
+            t = clip_lo0(x3 - g4 * r3, hi_of(x2));
+            s = t - x3; x3 = t;
+            g3 = h3 + t * G34; g4 = h4 + t * G44;
+            g0 += s * G04; g1 += s * G14;
+        }
+#else
         t = clip_lo0(x2 - g3 * r2, hi_of(x3));
         s = t - x2; x2 = t;
         g0 += s * G03; g1 += s * G13; g3 += s * G33; g4 += s * G34;
         t = clip_lo0(x3 - g4 * r3, hi_of(x2));
         s = t - x3; x3 = t;
         g0 += s * G04; g1 += s * G14; g3 += s * G34; g4 += s * G44;
+#endif
         t = -(g4 - g3) * r3b;
         t = BOX ? clip_sym(t, x3, x2) : clipv(t, -maxv(x3, R(0)), maxv(x2, R(0)));
         x2 = x2 - t; x3 = x3 + t;
