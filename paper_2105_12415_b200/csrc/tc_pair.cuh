@@ -717,17 +717,16 @@ __device__ __forceinline__ void iterative_pair(const R* A, const R* B, R eps, co
 // slide gradients follow from e3a = E1 - E0 and -e3b = E4 - E3.  d itself
 // is rebuilt exactly from x where the settle test needs it.  Equal to the
 // reference up to rounding (checked within the north-star tolerance).
-template <bool BOX, class R, class Reload>
-__device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, const KP<R>& kp, Rec<R>& o,
-                                                    Reload reload) {
-    using T = typename Store<R>::type;
-    const R tiny = R(Tiny<R>::v);
-    const R half = R(T(0.5));
+template <bool BOX, class R>
+struct GramSolver {
     R G00, G01, G03, G04, G11, G13, G14, G33, G34, G44, SA0, SA1, SA3, SA4, SB0, SB1, SB3, SB4;
     R r0, r1, r2, r3, r3a, r3b;
-    R x0 = kp.start_coord, x1 = kp.start_coord, x2 = kp.start_coord, x3 = kp.start_coord;
+    R x0, x1, x2, x3;
     R g0, g1, g3, g4;
-    {
+
+    __device__ __forceinline__ void init(const R* A, const R* B, const KP<R>& kp) {
+        const R tiny = R(Tiny<R>::v);
+        x0 = x1 = x2 = x3 = kp.start_coord;
         R E0[3], E1[3], E3[3], E4[3], SA[3], SB[3], d[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -755,120 +754,98 @@ __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, cons
         for (int i = 0; i < 3; ++i) d[i] = (A[i] - B[i]) + x0 * E0[i] + x1 * E1[i] + x2 * E3[i] + x3 * E4[i];
         g0 = dot3(d, E0); g1 = dot3(d, E1); g3 = dot3(d, E3); g4 = dot3(d, E4);
     }
+
     // BOX (start_coord in [0, 1], the usual case): the iterates never leave
     // the box, so the inner max() of the clips are identities (coord_step)
-    auto hi_of = [&](R xp) { return BOX ? R(1) - xp : maxv(R(0), R(1) - maxv(xp, R(0))); };
-    auto clip_lo0 = [&](R v, R hi) { return clip0_hi(v, hi); };
-#ifndef TC_HTRICK
-#define TC_HTRICK 0
-#endif
-    auto sweep = [&]() {
+    __device__ __forceinline__ R hi_of(R xp) const { return BOX ? R(1) - xp : maxv(R(0), R(1) - maxv(xp, R(0))); }
+
+    __device__ __forceinline__ void sweep() {
         R t, s;
-#if TC_HTRICK
-        // the gradient the next substep reads is formed as t*G + (g - x*G),
-        // the bracket computed while the clip is still pending: the step's
-        // DADD leaves the dependent chain (one extra FMA per critical g)
-        {
-            const R h1 = g1 - x0 * G01;
-            t = clip_lo0(x0 - g0 * r0, hi_of(x1));
-            s = t - x0; x0 = t;
-            g1 = h1 + t * G01;
-            g0 += s * G00; g3 += s * G03; g4 += s * G04;
-        }
-        {
-            const R h0 = g0 - x1 * G01, h1 = g1 - x1 * G11;
-            t = clip_lo0(x1 - g1 * r1, hi_of(x0));
-            s = t - x1; x1 = t;
-            g0 = h0 + t * G01; g1 = h1 + t * G11;
-            g3 += s * G13; g4 += s * G14;
-        }
-#else
-        t = clip_lo0(x0 - g0 * r0, hi_of(x1));
+        t = clip0_hi(x0 - g0 * r0, hi_of(x1));
         s = t - x0; x0 = t;
         g0 += s * G00; g1 += s * G01; g3 += s * G03; g4 += s * G04;
-        t = clip_lo0(x1 - g1 * r1, hi_of(x0));
+        t = clip0_hi(x1 - g1 * r1, hi_of(x0));
         s = t - x1; x1 = t;
         g0 += s * G01; g1 += s * G11; g3 += s * G13; g4 += s * G14;
-#endif
         t = -(g1 - g0) * r3a;
         t = BOX ? clip_sym(t, x1, x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
         x0 = x0 - t; x1 = x1 + t;
         g0 += t * SA0; g1 += t * SA1; g3 += t * SA3; g4 += t * SA4;
-#if TC_HTRICK
-        {
-            const R h4 = g4 - x2 * G34;
-            t = clip_lo0(x2 - g3 * r2, hi_of(x3));
-            s = t - x2; x2 = t;
-            g4 = h4 + t * G34;
-            g0 += s * G03; g1 += s * G13; g3 += s * G33;
-        }
-        {
-            const R h3 = g3 - x3 * G34, h4 = g4 - x3 * G44;
-            t = clip_lo0(x3 - g4 * r3, hi_of(x2));
-            s = t - x3; x3 = t;
-            g3 = h3 + t * G34; g4 = h4 + t * G44;
-            g0 += s * G04; g1 += s * G14;
-        }
-#else
-        t = clip_lo0(x2 - g3 * r2, hi_of(x3));
+        t = clip0_hi(x2 - g3 * r2, hi_of(x3));
         s = t - x2; x2 = t;
         g0 += s * G03; g1 += s * G13; g3 += s * G33; g4 += s * G34;
-        t = clip_lo0(x3 - g4 * r3, hi_of(x2));
+        t = clip0_hi(x3 - g4 * r3, hi_of(x2));
         s = t - x3; x3 = t;
         g0 += s * G04; g1 += s * G14; g3 += s * G34; g4 += s * G44;
-#endif
         t = -(g4 - g3) * r3b;
         t = BOX ? clip_sym(t, x3, x2) : clipv(t, -maxv(x3, R(0)), maxv(x2, R(0)));
         x2 = x2 - t; x3 = x3 + t;
         g0 += t * SB0; g1 += t * SB1; g3 += t * SB3; g4 += t * SB4;
-    };
-    const int n_it = kp.n_iterative;
-#pragma unroll 1
-    for (int it = 0; it < n_it - 1; ++it) sweep();
-    // epilogue: re-read the pair (L1/L2 hit) and rebuild d exactly from x,
-    // once for the second-to-last sweep and once for the last, so nothing
-    // but x, g and the Gram terms is live across a sweep
-    R A0[3], B0[3], E0[3], E1[3], E3[3], E4[3], d[3];
-    auto diff = [&]() {
+    }
+
+    // epilogue: re-read the pair (shared-memory copy) and rebuild d exactly
+    // from x, once before the last sweep (prelast) and once after (finish),
+    // so nothing but x, g and the Gram terms is live across a sweep; the
+    // penalty weight and the halo are re-derived rather than kept live.
+    struct Pre { R j_old, mid_old[3], alpha_it, eps; };
+
+    template <class Reload>
+    __device__ __forceinline__ void prelast(Reload& reload, const KP<R>& kp, Pre& pre) const {
+        using T = typename Store<R>::type;
+        R A0[3], B0[3], E0[3], E1[3], E3[3], E4[3], d[3], sq;
+        reload(A0, B0, E0, E1, E3, E4, &sq, &pre.eps);
+        pre.alpha_it = kp.alpha_it * sq;
 #pragma unroll
         for (int i = 0; i < 3; ++i) d[i] = (A0[i] - B0[i]) + x0 * E0[i] + x1 * E1[i] + x2 * E3[i] + x3 * E4[i];
-    };
-    // the penalty weight and the halo are re-derived here rather than kept
-    // live through the sweep loop (register pressure)
-    R j_old, mid_old[3], alpha_it, eps;
-    {
-        R sq;
-        reload(A0, B0, E0, E1, E3, E4, &sq, &eps);
-        alpha_it = kp.alpha_it * sq;
-        diff();
-        R xs[4] = {x0, x1, x2, x3};
-        j_old = half * dot3(d, d) + penalty(xs, alpha_it);
-        contact_mid(A0, xs, E0, E1, d, mid_old);
+        const R xs[4] = {x0, x1, x2, x3};
+        pre.j_old = R(T(0.5)) * dot3(d, d) + penalty(xs, pre.alpha_it);
+        contact_mid(A0, xs, E0, E1, d, pre.mid_old);
     }
-    sweep();
-    reload(A0, B0, E0, E1, E3, E4, nullptr, nullptr);
-    diff();
-    R xs[4] = {x0, x1, x2, x3};
-    const R dd = dot3(d, d);
-    const R j_total = half * dd + penalty(xs, alpha_it);
-    R mv[3];
-    contact_mid(A0, xs, E0, E1, d, mv);
+
+    template <class Reload>
+    __device__ __forceinline__ void finish(Reload& reload, const KP<R>& kp, const Pre& pre, Rec<R>& o) const {
+        using T = typename Store<R>::type;
+        const R half = R(T(0.5));
+        R A0[3], B0[3], E0[3], E1[3], E3[3], E4[3], d[3];
+        reload(A0, B0, E0, E1, E3, E4, nullptr, nullptr);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) mv[i] = mv[i] - mid_old[i];
-    const R move = sqrtv(norm3_sq_sum(mv));
-    const R jh = half * dd;
-    const bool settled = (absv(j_total - j_old) <= kp.c_factor * eps) && (move <= kp.move_factor * eps);
-    const bool contact = settled && (jh <= (R(T(2)) * eps) * eps);
-    o.kind = contact ? KIND_CONTACT : (settled ? KIND_NO_CONTACT : KIND_NOT_TERMINATED);
+        for (int i = 0; i < 3; ++i) d[i] = (A0[i] - B0[i]) + x0 * E0[i] + x1 * E1[i] + x2 * E3[i] + x3 * E4[i];
+        const R xs[4] = {x0, x1, x2, x3};
+        const R dd = dot3(d, d);
+        const R j_total = half * dd + penalty(xs, pre.alpha_it);
+        R mv[3];
+        contact_mid(A0, xs, E0, E1, d, mv);
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        o.pa[i] = (A0[i] + x0 * E0[i]) + x1 * E1[i];
-        o.pb[i] = (B0[i] - x2 * E3[i]) - x3 * E4[i];
+        for (int i = 0; i < 3; ++i) mv[i] = mv[i] - pre.mid_old[i];
+        const R move = sqrtv(norm3_sq_sum(mv));
+        const R jh = half * dd;
+        const R eps = pre.eps;
+        const bool settled = (absv(j_total - pre.j_old) <= kp.c_factor * eps) && (move <= kp.move_factor * eps);
+        const bool contact = settled && (jh <= (R(T(2)) * eps) * eps);
+        o.kind = contact ? KIND_CONTACT : (settled ? KIND_NO_CONTACT : KIND_NOT_TERMINATED);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            o.pa[i] = (A0[i] + x0 * E0[i]) + x1 * E1[i];
+            o.pb[i] = (B0[i] - x2 * E3[i]) - x3 * E4[i];
+        }
+        o.distance = sqrtv(R(T(2)) * jh);
+        o.ba[0] = x0; o.ba[1] = x1;
+        o.bb[0] = x2; o.bb[1] = x3;
+        o.ids = 0x00FFFFFFu | ((uint32_t)((settled ? FLAG_SETTLED : 0u) | (contact ? FLAG_ITER_CONTACT : 0u)) << 24);
     }
-    o.distance = sqrtv(R(T(2)) * jh);
-    o.ba[0] = x0; o.ba[1] = x1;
-    o.bb[0] = x2; o.bb[1] = x3;
-    o.ids = 0x00FFFFFFu | ((uint32_t)((settled ? FLAG_SETTLED : 0u) | (contact ? FLAG_ITER_CONTACT : 0u)) << 24);
+};
+
+template <bool BOX, class R, class Reload>
+__device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, const KP<R>& kp, Rec<R>& o,
+                                                    Reload reload) {
+    GramSolver<BOX, R> gs;
+    gs.init(A, B, kp);
+#pragma unroll 1
+    for (int it = 0; it < kp.n_iterative - 1; ++it) gs.sweep();
+    typename GramSolver<BOX, R>::Pre pre;
+    gs.prelast(reload, kp, pre);
+    gs.sweep();
+    gs.finish(reload, kp, pre, o);
 }
 
 }  // namespace tc
