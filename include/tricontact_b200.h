@@ -137,7 +137,10 @@ int tc_degenerate_mask_f64(const double* tris, int64_t n, uint8_t* mask, void* s
 int tc_degenerate_mask_f32(const float* tris, int64_t n, uint8_t* mask, void* stream);
 
 /* ---- all-pairs particle blocks (BASELINE.json config 2) -------------------
- * meshes: [n_meshes][tris_per_mesh][9] world-space triangles (device);
+ * meshes: [n_meshes][tris_per_mesh][9] world-space triangles (device), or
+ * local-space ones when motions ([n_meshes][7]: unit quaternion w, x, y, z and
+ * translation, RK/geometry.py:124-176) is given -- the rigid motion is then
+ * applied while the mesh is staged (fused transform, no world-space copy);
  * blocks: [n_blocks][2] int32 mesh indices; every block runs the hybrid kernel
  * on all tris_per_mesh^2 triangle pairs (mesh A's triangle i, mesh B's j),
  * both meshes staged in shared memory -- the all-pairs meshgrid of
@@ -148,13 +151,13 @@ int tc_degenerate_mask_f32(const float* tris, int64_t n, uint8_t* mask, void* st
  * all contacts, also those beyond max_contacts.  tc_stats tallies every pair.
  * Degenerate fallback pairs are counted in stats->degenerate, never listed. */
 int tc_blocks_hybrid_f64(const double* meshes, int32_t tris_per_mesh, int64_t n_meshes,
-                         const int32_t* blocks, int64_t n_blocks, const double* block_eps,
+                         const double* motions, const int32_t* blocks, int64_t n_blocks, const double* block_eps,
                          const tc_params* p, int64_t max_contacts, int32_t* contact_idx,
                          double* contact_distance, double* contact_point_a,
                          double* contact_point_b, int64_t* n_contacts, tc_stats* stats,
                          void* stream);
 int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_meshes,
-                         const int32_t* blocks, int64_t n_blocks, const float* block_eps,
+                         const float* motions, const int32_t* blocks, int64_t n_blocks, const float* block_eps,
                          const tc_params* p, int64_t max_contacts, int32_t* contact_idx,
                          float* contact_distance, float* contact_point_a,
                          float* contact_point_b, int64_t* n_contacts, tc_stats* stats,

@@ -580,7 +580,8 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
 
 template <typename T>
 struct BlockArgs {
-    const T* meshes;          // [n_meshes][tris][9], world coordinates
+    const T* meshes;          // [n_meshes][tris][9]: world coordinates, or local ones with motions
+    const T* motions;         // [n_meshes][7] (qw, qx, qy, qz, tx, ty, tz) or NULL
     int tris;
     int64_t n_meshes;
     const int32_t* blocks;    // [nb][2] mesh indices (A, B)
@@ -597,6 +598,33 @@ struct BlockArgs {
     double c_factor, alpha_it, alpha_reg, move_factor, start_coord;
     int n_iterative;
 };
+
+// RK/geometry.py:162-171 rotation_matrix of the unit quaternion (w, x, y, z),
+// evaluated in double like the reference's Python floats, then rounded to T.
+template <class R, typename T>
+__device__ __forceinline__ void motion_matrix(const T* m, R* Rm, R* tr) {
+    const double w = m[0], x = m[1], y = m[2], z = m[3];
+    const double v[9] = {1.0 - 2.0 * (__dadd_rn(__dmul_rn(y, y), __dmul_rn(z, z))),
+                         2.0 * __dsub_rn(__dmul_rn(x, y), __dmul_rn(w, z)),
+                         2.0 * __dadd_rn(__dmul_rn(x, z), __dmul_rn(w, y)),
+                         2.0 * __dadd_rn(__dmul_rn(x, y), __dmul_rn(w, z)),
+                         1.0 - 2.0 * (__dadd_rn(__dmul_rn(x, x), __dmul_rn(z, z))),
+                         2.0 * __dsub_rn(__dmul_rn(y, z), __dmul_rn(w, x)),
+                         2.0 * __dsub_rn(__dmul_rn(x, z), __dmul_rn(w, y)),
+                         2.0 * __dadd_rn(__dmul_rn(y, z), __dmul_rn(w, x)),
+                         1.0 - 2.0 * (__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)))};
+#pragma unroll
+    for (int k = 0; k < 9; ++k) Rm[k] = R(T(v[k]));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) tr[k] = R(m[4 + k]);
+}
+
+// world = R p + t, row by row: ((R_i0 p0 + R_i1 p1) + R_i2 p2) + t_i
+template <class R>
+__device__ __forceinline__ void apply_motion(const R* Rm, const R* tr, const R* p, R* w) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) w[i] = ((Rm[3 * i] * p[0] + Rm[3 * i + 1] * p[1]) + Rm[3 * i + 2] * p[2]) + tr[i];
+}
 
 template <class R, typename T>
 struct BlockSource {
@@ -649,10 +677,34 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) blocks_hybrid_kernel(Bl
         const int64_t ia = a.blocks[2 * blk], ib = a.blocks[2 * blk + 1];
         const T* gA = a.meshes + ia * tris * 9;
         const T* gB = a.meshes + ib * tris * 9;
-        for (int e = threadIdx.x; e < 9 * tris; e += BLOCK) {
-            const int t = e / 9, c = e - 9 * (e / 9);
-            mA[c * tris + t] = __ldg(gA + e);
-            mB[c * tris + t] = __ldg(gB + e);
+        if (a.motions) {
+            // rigid motion fused into the staging (RK/stepping.py:157-159,
+            // 290-291: Particle.world_tris = motion.apply_points(local))
+            R RA[9], tA[3], RB[9], tB[3];
+            motion_matrix(a.motions + 7 * ia, RA, tA);
+            motion_matrix(a.motions + 7 * ib, RB, tB);
+            for (int e = threadIdx.x; e < 3 * tris; e += BLOCK) {
+                const int t = e / 3, v = e - 3 * (e / 3);
+                R pa[3], pb[3], wa[3], wb[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    pa[c] = R(__ldg(gA + 3 * e + c));
+                    pb[c] = R(__ldg(gB + 3 * e + c));
+                }
+                apply_motion(RA, tA, pa, wa);
+                apply_motion(RB, tB, pb, wb);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    mA[(3 * v + c) * tris + t] = val(wa[c]);
+                    mB[(3 * v + c) * tris + t] = val(wb[c]);
+                }
+            }
+        } else {
+            for (int e = threadIdx.x; e < 9 * tris; e += BLOCK) {
+                const int t = e / 9, c = e - 9 * (e / 9);
+                mA[c * tris + t] = __ldg(gA + e);
+                mB[c * tris + t] = __ldg(gB + e);
+            }
         }
         if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
         __syncthreads();
@@ -838,7 +890,8 @@ static int run_device(int variant, const T* tri_a, const T* tri_b, int64_t n, co
 }
 
 template <typename T>
-static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const int32_t* blocks, int64_t nb,
+static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const T* motions, const int32_t* blocks,
+                      int64_t nb,
                       const T* block_eps, const tc_params* p, int64_t max_contacts, int32_t* c_idx, T* c_dist,
                       T* c_pa, T* c_pb, int64_t* n_contacts, tc_stats* stats, void* stream) {
     if (!params_ok(p) || nb < 0 || tris < 1 || n_meshes < 1 || max_contacts < 0 || !n_contacts ||
@@ -854,7 +907,7 @@ static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const int
         return TC_EINVAL;
     }
     BlockArgs<T> a;
-    a.meshes = meshes; a.tris = tris; a.n_meshes = n_meshes; a.blocks = blocks; a.nb = nb;
+    a.meshes = meshes; a.motions = motions; a.tris = tris; a.n_meshes = n_meshes; a.blocks = blocks; a.nb = nb;
     a.block_eps = block_eps; a.eps_scalar = (T)p->epsilon; a.max_contacts = max_contacts;
     a.c_idx = c_idx; a.c_dist = c_dist; a.c_pa = c_pa; a.c_pb = c_pb;
     a.n_contacts = reinterpret_cast<unsigned long long*>(n_contacts);
@@ -1155,19 +1208,21 @@ int tc_degenerate_mask_host_f32(const float* tris, int64_t n, uint8_t* mask) {
     return tc::run_degenerate_host<float>(tris, n, mask);
 }
 
-int tc_blocks_hybrid_f64(const double* meshes, int32_t tris_per_mesh, int64_t n_meshes, const int32_t* blocks,
+int tc_blocks_hybrid_f64(const double* meshes, int32_t tris_per_mesh, int64_t n_meshes, const double* motions,
+                         const int32_t* blocks,
                          int64_t n_blocks, const double* block_eps, const tc_params* p, int64_t max_contacts,
                          int32_t* contact_idx, double* contact_distance, double* contact_point_a,
                          double* contact_point_b, int64_t* n_contacts, tc_stats* stats, void* stream) {
-    return tc::run_blocks<double>(meshes, tris_per_mesh, n_meshes, blocks, n_blocks, block_eps, p, max_contacts,
+    return tc::run_blocks<double>(meshes, tris_per_mesh, n_meshes, motions, blocks, n_blocks, block_eps, p, max_contacts,
                                   contact_idx, contact_distance, contact_point_a, contact_point_b, n_contacts,
                                   stats, stream);
 }
-int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_meshes, const int32_t* blocks,
+int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_meshes, const float* motions,
+                         const int32_t* blocks,
                          int64_t n_blocks, const float* block_eps, const tc_params* p, int64_t max_contacts,
                          int32_t* contact_idx, float* contact_distance, float* contact_point_a,
                          float* contact_point_b, int64_t* n_contacts, tc_stats* stats, void* stream) {
-    return tc::run_blocks<float>(meshes, tris_per_mesh, n_meshes, blocks, n_blocks, block_eps, p, max_contacts,
+    return tc::run_blocks<float>(meshes, tris_per_mesh, n_meshes, motions, blocks, n_blocks, block_eps, p, max_contacts,
                                  contact_idx, contact_distance, contact_point_a, contact_point_b, n_contacts, stats,
                                  stream);
 }

@@ -97,6 +97,43 @@ def cfg2_scene(grid=(16, 16, 8), level: int = 2, seed: int = 2, jitter: float = 
     return np.ascontiguousarray(meshes), pairs[keep].astype(np.int32), gaps[keep]
 
 
+def rotation_matrix_ref(q):
+    """RK/geometry.py:162-171 for one unit quaternion, in Python floats."""
+    w, x, y, z = (float(c) for c in q)
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+def apply_motion_ref(local: np.ndarray, motion: np.ndarray) -> np.ndarray:
+    """World coordinates in the kernel's fused-transform order,
+    ((R_i0 p0 + R_i1 p1) + R_i2 p2) + t_i (elementwise, no FMA)."""
+    R = rotation_matrix_ref(motion[:4]).astype(local.dtype)
+    t = np.asarray(motion[4:7], local.dtype)
+    p = local.reshape(-1, 3)
+    w = np.empty_like(p)
+    for i in range(3):
+        w[:, i] = ((R[i, 0] * p[:, 0] + R[i, 1] * p[:, 1]) + R[i, 2] * p[:, 2]) + t[i]
+    return w.reshape(local.shape)
+
+
+def cfg2_scene_local(**kw):
+    """cfg2 as local-space meshes + rigid motions (N, 7): each particle's
+    jittered mesh centred at the origin, rotated and translated by its motion."""
+    rng = np.random.default_rng(kw.pop("seed", 2))
+    meshes, blocks, gaps = cfg2_scene(seed=int(rng.integers(1 << 30)), **kw)
+    N = meshes.shape[0]
+    centers = meshes.reshape(N, -1, 3).mean(axis=1)
+    local = meshes - centers[:, None, None, :]
+    q = rng.normal(size=(N, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    Rt = rotation_matrices(q)
+    # local = R^T (world - c): the motion (q, c) maps it back near the world pose
+    local = np.einsum("nji,ntvj->ntvi", Rt, local)
+    motions = np.concatenate([q, centers], axis=1)
+    return np.ascontiguousarray(local), motions, blocks, gaps
+
+
 def block_pairs(meshes: np.ndarray, blocks: np.ndarray, which):
     """Materialise the (A, B) triangle pairs of the listed blocks (oracle checks):
     pair (i, j) of block b is at row b_pos * T * T + i * T + j."""
@@ -109,11 +146,13 @@ def block_pairs(meshes: np.ndarray, blocks: np.ndarray, which):
     return np.concatenate(As), np.concatenate(Bs)
 
 
-def blocks_hybrid(meshes, blocks, params, *, block_eps=None, strict=False, max_contacts=1 << 20,
+def blocks_hybrid(meshes, blocks, params, *, motions=None, block_eps=None, strict=False, max_contacts=1 << 20,
                   stats=None, stream=None):
     """Hybrid kernel over every triangle pair of every block (device tensors).
 
-    ``meshes``: (N, T, 3, 3) CUDA tensor; ``blocks``: (nb, 2) int32 CUDA tensor.
+    ``meshes``: (N, T, 3, 3) CUDA tensor (world space, or local space with
+    ``motions`` (N, 7) = quaternion (w, x, y, z) + translation, applied while
+    the meshes are staged); ``blocks``: (nb, 2) int32 CUDA tensor.
     Returns a dict: n_contacts (device int64 scalar tensor) and the contact
     arrays idx (max, 3) int32 [block, tri_a, tri_b], distance, point_a, point_b
     (unordered; ``sort_contacts`` orders them like the reference).
@@ -136,8 +175,10 @@ def blocks_hybrid(meshes, blocks, params, *, block_eps=None, strict=False, max_c
     st = stream if stream is not None else torch.cuda.current_stream(dev)
     if block_eps is not None:
         block_eps = block_eps.to(device=dev, dtype=dt).contiguous()
+    if motions is not None:
+        motions = motions.to(device=dev, dtype=dt).contiguous()
     fn = getattr(_abi.load(), f"tc_blocks_hybrid_{_DT[dt]}")
-    rc = fn(_p(meshes), int(meshes.shape[1]), int(meshes.shape[0]), _p(blocks), int(blocks.shape[0]),
+    rc = fn(_p(meshes), int(meshes.shape[1]), int(meshes.shape[0]), _p(motions), _p(blocks), int(blocks.shape[0]),
             _p(block_eps), ctypes.byref(p), int(max_contacts), _p(out["idx"]), _p(out["distance"]),
             _p(out["point_a"]), _p(out["point_b"]), _p(out["n_contacts"]), _p(stats),
             ctypes.c_void_p(st.cuda_stream))

@@ -96,3 +96,34 @@ def test_blocks_contact_capacity_and_empty(scene):
     empty = PT.blocks_hybrid(torch.from_numpy(meshes).cuda(), torch.zeros((0, 2), dtype=torch.int32).cuda(),
                              D.Params())
     assert int(empty["n_contacts"].item()) == 0
+
+
+@pytest.mark.parametrize("strict", [True, False])
+def test_blocks_fused_rigid_motion(oracle_lib, strict):
+    """Local-space meshes + per-particle rigid motions, transformed while the
+    meshes are staged, equal the world-space run."""
+    local, motions, blocks, gaps = PT.cfg2_scene_local(grid=(4, 4, 2))
+    world = np.stack([PT.apply_motion_ref(local[k], motions[k]) for k in range(local.shape[0])])
+    which = [int(b) for b in np.argsort(gaps)[:3]]
+    pk = dict(epsilon=5e-2)
+    st1, st2 = D.new_stats(), D.new_stats()
+    fused = PT.blocks_hybrid(torch.from_numpy(local).cuda(), torch.from_numpy(blocks[which]).cuda(), D.Params(**pk),
+                             motions=torch.from_numpy(motions).cuda(), strict=strict, stats=st1)
+    plain = PT.blocks_hybrid(torch.from_numpy(world).cuda(), torch.from_numpy(blocks[which]).cuda(), D.Params(**pk),
+                             strict=strict, stats=st2)
+    torch.cuda.synchronize()
+    a, b = PT.sort_contacts(fused), PT.sort_contacts(plain)
+    assert a["n_contacts"] == b["n_contacts"] > 0
+    assert np.array_equal(a["idx"], b["idx"])
+    if strict:   # the fused transform rounds exactly like apply_motion_ref
+        for k in ("distance", "point_a", "point_b"):
+            assert np.array_equal(a[k], b[k]), k
+        assert D.read_stats(st1) == D.read_stats(st2)
+    else:        # FMA-contracted transform: last-bit differences only
+        for k in ("distance", "point_a", "point_b"):
+            assert np.allclose(a[k], b[k], rtol=0, atol=1e-13), k
+    if strict:
+        A, B = PT.block_pairs(world, blocks, which)
+        p = oracle_lib.make_params(**pk)
+        ref, _, _ = oracle_lib.hybrid(A, B, p, p.epsilon, threads=oracle_lib.default_threads())
+        assert a["n_contacts"] == int((ref["kind"] == 1).sum())
