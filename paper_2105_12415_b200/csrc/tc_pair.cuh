@@ -408,7 +408,7 @@ __device__ __forceinline__ bool comparison_phase1(const Tri& A, const Tri& B, R 
 // and its region / segment-branch code; with `ids_only` (an intersecting
 // pair whose ids were requested) nothing else is written.
 template <class R, class Tri>
-__device__ __forceinline__ void comparison_phase2(const Tri& A, const Tri& B, R eps, bool ids_only, Rec<R>& o) {
+__device__ __forceinline__ void comparison_phase2_impl(const Tri& A, const Tri& B, R eps, bool ids_only, Rec<R>& o) {
     using T = typename Store<R>::type;
     const R tiny = R(Tiny<R>::v);
     int best_row = 0, best_code = 0;
@@ -496,6 +496,28 @@ __device__ __forceinline__ void comparison_phase2(const Tri& A, const Tri& B, R 
     }
     o.kind = (o.distance <= R(T(2)) * eps) ? KIND_CONTACT : KIND_NO_CONTACT;
     o.ids |= 255u << 16;
+}
+
+// Phase 2 entry: the 15 tests re-read the pair's vertices many times, so
+// with TC_P2_REGS the pair is first copied from its shared-memory slot into
+// registers (phase 2 no longer shares the register file with the crossing
+// list or the iterative state).
+#ifndef TC_P2_REGS
+#define TC_P2_REGS 0  // measured slower (spills at the 128-register cap): off
+#endif
+template <class R, class Tri>
+__device__ __forceinline__ void comparison_phase2(const Tri& A, const Tri& B, R eps, bool ids_only, Rec<R>& o) {
+#if TC_P2_REGS
+    R a[9], b[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        a[k] = A[k];
+        b[k] = B[k];
+    }
+    comparison_phase2_impl(RegTri<R>{a}, RegTri<R>{b}, eps, ids_only, o);
+#else
+    comparison_phase2_impl(A, B, eps, ids_only, o);
+#endif
 }
 
 // RK/kernels.py:417-431 _penalty_value, summed left to right.
