@@ -163,6 +163,40 @@ int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_m
                          float* contact_point_b, int64_t* n_contacts, tc_stats* stats,
                          void* stream);
 
+/* ---- multiscale frontier traversal ---------------------
+ * RK/stepping.py:311-368 multiscale_contacts for n_pairs particle pairs at
+ * once.  The surrogate trees of all particles are concatenated FlatTree arrays
+ * (RK/stepping.py:78-129) under one global id space (DEVICE pointers):
+ * tris [n_total][9] world coordinates, node_eps [n_total], child_off
+ * [n_total + 1] / child_ids (CSR children, global ids; a leaf node lists its
+ * mesh triangles), is_fine [n_total] (1 = mesh triangle), height [n_total]
+ * (0 = mesh level).  roots: HOST [n_pairs][2] global root ids (i, j).
+ * Every round runs the hybrid kernel on the frontier with the halo
+ * 0.5 (eps_i + eps_j) and the comparison fallback only on mesh-level pairs,
+ * then unfolds contact/unsettled non-mesh pairings into the meshgrid of their
+ * children (a mesh-level side stays itself).  Mesh-level contacts are
+ * appended (unordered) to contact_idx [max][3] = (pair, id_i, id_j) and
+ * contact_point_a/b [max][3] (device); *n_contacts (HOST) counts all of them,
+ * also those beyond max_contacts.  checks (HOST, may be NULL)
+ * [max_height + 1] accumulates the pairings per max(height_i, height_j)
+ * (StepStats.record_checks); stats (HOST, may be NULL) accumulates the
+ * kernel tallies.  TC_EDEGENERATE when a mesh-level fallback pair holds a
+ * degenerate triangle (the reference raises DegenerateTriangle).  Params
+ * flags: TC_STRICT only.  Synchronous on `stream` (one 8-byte read-back per
+ * round). */
+int tc_multiscale_f64(const double* tris, const double* node_eps, const int32_t* child_off,
+                      const int32_t* child_ids, const uint8_t* is_fine, const int32_t* height,
+                      int32_t max_height, const int32_t* roots, int64_t n_pairs, const tc_params* p,
+                      int64_t max_contacts, int32_t* contact_idx, double* contact_point_a,
+                      double* contact_point_b, int64_t* n_contacts, int64_t* checks, tc_stats* stats,
+                      void* stream);
+int tc_multiscale_f32(const float* tris, const float* node_eps, const int32_t* child_off,
+                      const int32_t* child_ids, const uint8_t* is_fine, const int32_t* height,
+                      int32_t max_height, const int32_t* roots, int64_t n_pairs, const tc_params* p,
+                      int64_t max_contacts, int32_t* contact_idx, float* contact_point_a,
+                      float* contact_point_b, int64_t* n_contacts, int64_t* checks, tc_stats* stats,
+                      void* stream);
+
 /* ---- host entry points ----------------------------------------------------
  * Same arguments with HOST pointers; variant: 0 comparison, 1 iterative,
  * 2 hybrid.  stats (host, may be NULL) receives this call's tallies

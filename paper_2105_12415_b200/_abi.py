@@ -83,6 +83,11 @@ for _s in ("f64", "f32"):
     # n_contacts, stats, stream
     SIGNATURES[f"tc_blocks_hybrid_{_s}"] = (_INT, [_P, ctypes.c_int32, _I64, _P, _P, _I64, _P, _P, _I64] + [_P] * 7)
 
+for _s in ("f64", "f32"):
+    # tris, node_eps, child_off, child_ids, is_fine, height, max_height, roots, n_pairs, p, max_contacts,
+    # idx, pa, pb, n_contacts, checks, stats, stream
+    SIGNATURES[f"tc_multiscale_{_s}"] = (_INT, [_P] * 6 + [ctypes.c_int32, _P, _I64, _P, _I64] + [_P] * 7)
+
 _lib = None
 
 
@@ -121,3 +126,4 @@ def params_struct(params, flags: int = 0) -> TcParams:
     return TcParams(float(params.epsilon), float(params.c_factor), float(params.alpha_iterative),
                     float(params.alpha_regulariser), float(params.move_factor), float(params.start_coord),
                     int(params.n_iterative), int(flags))
+

@@ -19,6 +19,8 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <cub/device/device_scan.cuh>
+#include <vector>
 #include <mutex>
 
 #include "tc_pair.cuh"
@@ -747,6 +749,173 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) blocks_hybrid_kernel(Bl
     tl.flush<true>(a.stats);
 }
 
+// ---- multiscale frontier traversal ---------------------------
+// RK/stepping.py:311-368 multiscale_contacts on the device, for a batch of
+// particle pairs at once.  Trees are concatenated FlatTree arrays (surrogate
+// nodes and mesh triangles, RK/stepping.py:78-129) with global ids.  One
+// round = one hybrid launch over the frontier (per-pair halo 0.5 (eps_i +
+// eps_j), fallback only where both sides are mesh triangles -- the
+// reference's allow_fallback=both_fine), then the frontier is unfolded: a
+// pairing that is in contact or unsettled and not at mesh level on both sides
+// is replaced by the meshgrid of its children (a mesh-level side stays
+// itself); mesh-level contacts are appended to the contact list.
+
+template <typename T>
+struct FrontierArgs {
+    const T* tris;            // [n_total][9] world coordinates
+    const T* node_eps;        // [n_total]
+    const uint8_t* is_fine;   // [n_total]
+    const int32_t* height;    // [n_total]
+    const int32_t* fa;        // frontier: id on side i
+    const int32_t* fb;        // id on side j
+    const int32_t* ftag;      // particle-pair index
+    int64_t n;
+    int8_t* kind;             // [n] final kind per pairing
+    int64_t max_contacts;
+    int32_t* c_idx;           // [max][3] pair, id_i, id_j
+    T* c_pa;
+    T* c_pb;
+    unsigned long long* n_contacts;
+    unsigned long long* checks;  // [max_height + 1] pairings per max(height_i, height_j)
+    int max_height;
+    tc_stats* stats;
+    double c_factor, alpha_it, alpha_reg, move_factor, start_coord;
+    int n_iterative;
+};
+
+template <class R, typename T>
+struct FrontierSource {
+    const FrontierArgs<T>& a;
+    __device__ __forceinline__ bool want_ids() const { return false; }
+    __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
+        T* slot = thread_slot<T>(18 * BLOCK);
+        const int64_t ia = a.fa[j], ib = a.fb[j];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            slot[k * BLOCK] = __ldg(a.tris + 9 * ia + k);
+            slot[(9 + k) * BLOCK] = __ldg(a.tris + 9 * ib + k);
+        }
+        A.p = slot;
+        A.stride = BLOCK;
+        B.p = slot + 9 * BLOCK;
+        B.stride = BLOCK;
+        eps = R(T(0.5)) * (R(a.node_eps[ia]) + R(a.node_eps[ib]));
+    }
+    __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const {
+        a.kind[j] = (int8_t)r.kind;
+        if (r.kind != KIND_CONTACT) return;
+        const int64_t ia = a.fa[j], ib = a.fb[j];
+        if (!(a.is_fine[ia] && a.is_fine[ib])) return;
+        const unsigned long long slot = atomicAdd(a.n_contacts, 1ull);
+        if ((long long)slot >= a.max_contacts) return;
+        a.c_idx[3 * slot] = a.ftag[j];
+        a.c_idx[3 * slot + 1] = (int32_t)ia;
+        a.c_idx[3 * slot + 2] = (int32_t)ib;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            a.c_pa[3 * slot + c] = val(r.pa[c]);
+            a.c_pb[3 * slot + c] = val(r.pb[c]);
+        }
+    }
+    __device__ __forceinline__ void store_ids01(int64_t, uint32_t) const {}
+};
+
+template <typename T, bool STRICT>
+__global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) frontier_hybrid_kernel(FrontierArgs<T> a) {
+    using R = typename Pol<T, STRICT>::R;
+    __shared__ Queues Q;
+    __shared__ unsigned long long hist[32];
+    const KP<R> kp = make_kp<R>(a);
+    const FrontierSource<R, T> src{a};
+    Tally tl;
+    if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
+    if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t i = tile * BLOCK + threadIdx.x;
+        bool enq = false;
+        if (i < a.n) {
+            const int64_t ia = a.fa[i], ib = a.fb[i];
+            R A[9], B[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                A[k] = R(__ldg(a.tris + 9 * ia + k));
+                B[k] = R(__ldg(a.tris + 9 * ib + k));
+            }
+            T* slot = thread_slot<T>(18 * BLOCK);
+            stash_pair(slot, A, B);
+            const bool both_fine = a.is_fine[ia] && a.is_fine[ib];
+            const int h = max(a.height[ia], a.height[ib]);
+            atomicAdd(&hist[h < 31 ? h : 31], 1ull);
+            Rec<R> r;
+            run_iterative(slot, A, B,
+                          [&] { return R(T(0.5)) * (R(a.node_eps[ia]) + R(a.node_eps[ib])); }, kp, r);
+            tl.iterative++;
+            if (r.kind == KIND_NOT_TERMINATED && both_fine) {
+                const SmemTri<R> SA{slot, BLOCK}, SB{slot + 9 * BLOCK, BLOCK};
+                if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {
+                    r.kind = KIND_DEGENERATE;
+                    tl.degenerate++;
+                } else {
+                    enq = true;
+                }
+            }
+            if (!enq) {
+                src.store(i, r);
+                tl.result(r);
+            }
+        }
+        push(Q.q1, &Q.n1, enq, i);
+        __syncthreads();
+        drain<R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+    }
+    drain<R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    __syncthreads();
+    if (threadIdx.x <= (unsigned)a.max_height && threadIdx.x < 32 && hist[threadIdx.x])
+        atomicAdd(a.checks + threadIdx.x, hist[threadIdx.x]);
+    tl.flush<true>(a.stats);
+}
+
+// Unfolding: how many next-round pairings each pairing spawns.
+__global__ void frontier_count_kernel(const int8_t* kind, const int32_t* fa, const int32_t* fb, int64_t n,
+                                      const uint8_t* is_fine, const int32_t* child_off, int64_t* count) {
+    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < n; f += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t ia = fa[f], ib = fb[f];
+        const bool fi = is_fine[ia], fj = is_fine[ib];
+        const int k = kind[f];
+        int64_t c = 0;
+        if ((k == KIND_CONTACT || k == KIND_NOT_TERMINATED) && !(fi && fj)) {
+            const int64_t ni = fi ? 1 : child_off[ia + 1] - child_off[ia];
+            const int64_t nj = fj ? 1 : child_off[ib + 1] - child_off[ib];
+            c = ni * nj;
+        }
+        count[f] = c;
+    }
+}
+
+// Unfolding: write the children meshgrid (indexing "ij") of every spawning
+// pairing at its exclusive-scan offset.
+__global__ void frontier_write_kernel(const int32_t* fa, const int32_t* fb, const int32_t* ftag, int64_t n,
+                                      const int64_t* count, const int64_t* offset, const uint8_t* is_fine,
+                                      const int32_t* child_off, const int32_t* child_ids, int32_t* na, int32_t* nb,
+                                      int32_t* ntag) {
+    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < n; f += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = count[f];
+        if (!c) continue;
+        const int32_t ia = fa[f], ib = fb[f];
+        const bool fi = is_fine[ia], fj = is_fine[ib];
+        const int64_t nj = fj ? 1 : child_off[ib + 1] - child_off[ib];
+        const int64_t base = offset[f];
+        for (int64_t r = 0; r < c; ++r) {
+            const int64_t u = r / nj, v = r - u * nj;
+            na[base + r] = fi ? ia : child_ids[child_off[ia] + u];
+            nb[base + r] = fj ? ib : child_ids[child_off[ib] + v];
+            ntag[base + r] = ftag[f];
+        }
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(BLOCK) cpt_kernel(const T* P, const T* Tr, int64_t n, T* closest, T* bary) {
     using R = Strict<T>;
@@ -924,6 +1093,147 @@ static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const T* 
     g_launches++;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TC_OK : set_err("blocks launch", e);
+}
+
+// Host driver of the multiscale traversal: one hybrid launch + unfolding per
+// round, until the frontier is empty (one 8-byte read-back per round).
+template <typename T>
+static int run_multiscale(const T* tris, const T* node_eps, const int32_t* child_off, const int32_t* child_ids,
+                          const uint8_t* is_fine, const int32_t* height, int32_t max_height, const int32_t* roots,
+                          int64_t n_pairs, const tc_params* p, int64_t max_contacts, int32_t* c_idx, T* c_pa,
+                          T* c_pb, int64_t* n_contacts_host, int64_t* checks_host, tc_stats* stats_host,
+                          void* stream) {
+    if (!params_ok(p) || n_pairs < 0 || max_height < 0 || max_height > 31 || max_contacts < 0 ||
+        (p->flags & (TC_SOA | TC_EMIT_IDS)) || !n_contacts_host) {
+        snprintf(g_err, sizeof(g_err), "invalid argument (multiscale)");
+        return TC_EINVAL;
+    }
+    *n_contacts_host = 0;
+    if (n_pairs == 0) return TC_OK;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    // device scratch: frontier (two generations), kind, counts/offsets, tallies
+    struct Buf {
+        void* p = nullptr;
+        ~Buf() { if (p) cudaFree(p); }
+    };
+    Buf fr_cur, kbuf, cbuf, obuf, tallies, scan_tmp;
+    int64_t cap = n_pairs > 1024 ? n_pairs : 1024;
+    auto alloc = [&](Buf& b, size_t bytes) -> cudaError_t {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        return cudaMalloc(&b.p, bytes);
+    };
+    auto grow = [&](int64_t need) -> cudaError_t {
+        cudaError_t r = cudaSuccess;
+        if (need <= cap && kbuf.p) return r;
+        cap = need > 2 * cap ? need : 2 * cap;
+        if ((r = alloc(kbuf, cap)) != cudaSuccess) return r;
+        if ((r = alloc(cbuf, sizeof(int64_t) * (cap + 1))) != cudaSuccess) return r;
+        if ((r = alloc(obuf, sizeof(int64_t) * (cap + 1))) != cudaSuccess) return r;
+        return r;
+    };
+    if ((e = alloc(fr_cur, 3 * sizeof(int32_t) * cap)) != cudaSuccess) return set_err("cudaMalloc", e);
+    if ((e = grow(cap)) != cudaSuccess) return set_err("cudaMalloc", e);
+    // tallies: n_contacts, checks[32], stats
+    const size_t tb = sizeof(unsigned long long) * 33 + sizeof(tc_stats);
+    if ((e = alloc(tallies, tb)) != cudaSuccess) return set_err("cudaMalloc", e);
+    auto* d_nc = static_cast<unsigned long long*>(tallies.p);
+    auto* d_checks = d_nc + 1;
+    auto* d_stats = reinterpret_cast<tc_stats*>(d_checks + 32);
+    cudaMemsetAsync(tallies.p, 0, sizeof(unsigned long long) * 33, s);
+    stats_reset_kernel<<<1, 1, 0, s>>>(d_stats);
+    g_launches++;
+    // initial frontier: the roots
+    {
+        int32_t* fa = static_cast<int32_t*>(fr_cur.p);
+        std::vector<int32_t> h(3 * n_pairs);
+        for (int64_t k = 0; k < n_pairs; ++k) {
+            h[k] = roots[2 * k];
+            h[n_pairs + k] = roots[2 * k + 1];
+            h[2 * n_pairs + k] = (int32_t)k;
+        }
+        // planar: [fa | fb | tag] with stride = current frontier length
+        cudaMemcpyAsync(fa, h.data(), sizeof(int32_t) * 3 * n_pairs, cudaMemcpyHostToDevice, s);
+        cudaStreamSynchronize(s);
+    }
+    int64_t n = n_pairs;
+    const size_t smem = scratch_bytes<T>();
+    size_t scan_bytes = 0;
+    while (n > 0) {
+        if ((e = grow(n)) != cudaSuccess) return set_err("cudaMalloc", e);
+        int32_t* fa = static_cast<int32_t*>(fr_cur.p);
+        int32_t* fb = fa + n;
+        int32_t* ftag = fb + n;
+        FrontierArgs<T> a;
+        a.tris = tris; a.node_eps = node_eps; a.is_fine = is_fine; a.height = height;
+        a.fa = fa; a.fb = fb; a.ftag = ftag; a.n = n;
+        a.kind = static_cast<int8_t*>(kbuf.p);
+        a.max_contacts = max_contacts; a.c_idx = c_idx; a.c_pa = c_pa; a.c_pb = c_pb;
+        a.n_contacts = d_nc; a.checks = d_checks; a.max_height = max_height; a.stats = d_stats;
+        a.c_factor = p->c_factor; a.alpha_it = p->alpha_iterative; a.alpha_reg = p->alpha_regulariser;
+        a.move_factor = p->move_factor; a.start_coord = p->start_coord; a.n_iterative = p->n_iterative;
+        if (p->flags & TC_STRICT) {
+            auto k = frontier_hybrid_kernel<T, true>;
+            k<<<(unsigned)grid_for(k, n, smem), BLOCK, smem, s>>>(a);
+        } else {
+            auto k = frontier_hybrid_kernel<T, false>;
+            k<<<(unsigned)grid_for(k, n, smem), BLOCK, smem, s>>>(a);
+        }
+        g_launches++;
+        const unsigned g = (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+        int64_t* cnt = static_cast<int64_t*>(cbuf.p);
+        int64_t* off = static_cast<int64_t*>(obuf.p);
+        frontier_count_kernel<<<g, 256, 0, s>>>(a.kind, fa, fb, n, is_fine, child_off, cnt);
+        g_launches++;
+        size_t need = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, need, cnt, off, (int)(n + 1), s);
+        if (need > scan_bytes) {
+            if ((e = alloc(scan_tmp, need)) != cudaSuccess) return set_err("cudaMalloc", e);
+            scan_bytes = need;
+        }
+        // count[n] must be 0 for the (n+1)-long scan: the tail entry is the total
+        cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), s);
+        cub::DeviceScan::ExclusiveSum(scan_tmp.p, scan_bytes, cnt, off, (int)(n + 1), s);
+        g_launches++;
+        int64_t total = 0;
+        cudaMemcpyAsync(&total, off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err("multiscale round", e);
+        if (total > 0) {
+            Buf next;
+            if ((e = cudaMalloc(&next.p, 3 * sizeof(int32_t) * total)) != cudaSuccess) return set_err("cudaMalloc", e);
+            int32_t* na = static_cast<int32_t*>(next.p);
+            frontier_write_kernel<<<g, 256, 0, s>>>(fa, fb, ftag, n, cnt, off, is_fine, child_off, child_ids, na,
+                                                    na + total, na + 2 * total);
+            g_launches++;
+            if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err("multiscale unfold", e);
+            std::swap(fr_cur.p, next.p);
+        }
+        n = total;
+    }
+    unsigned long long h_nc = 0, h_checks[32];
+    tc_stats h_stats;
+    cudaMemcpy(&h_nc, d_nc, sizeof(h_nc), cudaMemcpyDeviceToHost);
+    cudaMemcpy(h_checks, d_checks, sizeof(h_checks), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&h_stats, d_stats, sizeof(h_stats), cudaMemcpyDeviceToHost);
+    if ((e = cudaGetLastError()) != cudaSuccess) return set_err("multiscale", e);
+    *n_contacts_host = (int64_t)h_nc;
+    if (checks_host)
+        for (int k = 0; k <= max_height; ++k) checks_host[k] += (int64_t)h_checks[k];
+    if (stats_host) {
+        stats_host->iterative += h_stats.iterative;
+        stats_host->comparison += h_stats.comparison;
+        stats_host->fallback += h_stats.fallback;
+        stats_host->degenerate += h_stats.degenerate;
+        stats_host->contacts += h_stats.contacts;
+        stats_host->intersecting += h_stats.intersecting;
+        if (h_stats.min_distance < stats_host->min_distance) stats_host->min_distance = h_stats.min_distance;
+    }
+    if (h_stats.degenerate > 0) {
+        snprintf(g_err, sizeof(g_err), "degenerate triangle in comparison fallback");
+        return TC_EDEGENERATE;
+    }
+    return TC_OK;
 }
 
 // ---- host pipeline ----------------------------------------------------------------------
@@ -1225,6 +1535,25 @@ int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_m
     return tc::run_blocks<float>(meshes, tris_per_mesh, n_meshes, motions, blocks, n_blocks, block_eps, p, max_contacts,
                                  contact_idx, contact_distance, contact_point_a, contact_point_b, n_contacts, stats,
                                  stream);
+}
+
+int tc_multiscale_f64(const double* tris, const double* node_eps, const int32_t* child_off, const int32_t* child_ids,
+                      const uint8_t* is_fine, const int32_t* height, int32_t max_height, const int32_t* roots,
+                      int64_t n_pairs, const tc_params* p, int64_t max_contacts, int32_t* contact_idx,
+                      double* contact_point_a, double* contact_point_b, int64_t* n_contacts, int64_t* checks,
+                      tc_stats* stats, void* stream) {
+    return tc::run_multiscale<double>(tris, node_eps, child_off, child_ids, is_fine, height, max_height, roots,
+                                      n_pairs, p, max_contacts, contact_idx, contact_point_a, contact_point_b,
+                                      n_contacts, checks, stats, stream);
+}
+int tc_multiscale_f32(const float* tris, const float* node_eps, const int32_t* child_off, const int32_t* child_ids,
+                      const uint8_t* is_fine, const int32_t* height, int32_t max_height, const int32_t* roots,
+                      int64_t n_pairs, const tc_params* p, int64_t max_contacts, int32_t* contact_idx,
+                      float* contact_point_a, float* contact_point_b, int64_t* n_contacts, int64_t* checks,
+                      tc_stats* stats, void* stream) {
+    return tc::run_multiscale<float>(tris, node_eps, child_off, child_ids, is_fine, height, max_height, roots,
+                                     n_pairs, p, max_contacts, contact_idx, contact_point_a, contact_point_b,
+                                     n_contacts, checks, stats, stream);
 }
 
 int tc_run_host_f64(int variant, const double* tri_a, const double* tri_b, int64_t n, const double* eps,

@@ -1,0 +1,105 @@
+"""Golden fixtures for the multiscale traversal.
+
+Runs in THIS container only: imports the read-only reference from
+/root/reference/pkg/src, builds its own two-particle scenes (the shapes of
+the reference's tests/test_stepping.py two_sphere_system and
+test_asymmetric_unfolding), runs tricontact.stepping.multiscale_contacts
+(RK/stepping.py:311-368) and single_level_contacts (:285-308) on them, and
+writes per-scene FlatTree arrays (world coordinates under the particle's
+motion, halos, children CSR, heights) with the reference's contacts, per-height
+check counts and kernel counters.
+
+    python tests/golden/make_multiscale_golden.py   # writes tests/golden/ms_float{64,32}.npz
+
+The float32 fixture is produced in a child interpreter with
+TRICONTACT_REAL=float32 (the reference fixes its scalar type at import).
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REF_SRC = Path("/root/reference/pkg/src")
+
+
+def _flat_arrays(particle, motion):
+    f = particle.flat
+    child_off = np.zeros(f.tri.shape[0] + 1, np.int32)
+    child_off[1:] = np.cumsum([c.size for c in f.children])
+    child_ids = np.concatenate([c for c in f.children if c.size]).astype(np.int32)
+    return dict(tris=particle.world_tris(motion).reshape(-1, 9), eps=f.eps.copy(), child_off=child_off,
+                child_ids=child_ids, height=f.height.astype(np.int32), n_nodes=np.int64(f.n_nodes))
+
+
+def _scene_out(prefix, system, out):
+    from tricontact.kernels import KernelParams
+    from tricontact.stepping import StepStats, multiscale_contacts, single_level_contacts
+
+    pi, pj = system.particles[0], system.particles[1]
+    params = KernelParams()
+    stats = StepStats()
+    multi = multiscale_contacts(pi, pj, (0, 1), params, stats)
+    single = single_level_contacts(pi, pj, (0, 1), params, StepStats())
+    for side, p in (("i", pi), ("j", pj)):
+        for k, v in _flat_arrays(p, p.motion).items():
+            out[f"{prefix}_{side}_{k}"] = v
+    out[f"{prefix}_source"] = np.array([c.source for c in multi], np.int64).reshape(-1, 2)
+    out[f"{prefix}_position"] = np.array([c.position for c in multi]).reshape(-1, 3)
+    out[f"{prefix}_normal"] = np.array([c.normal for c in multi]).reshape(-1, 3)
+    out[f"{prefix}_eps"] = np.array([c.eps for c in multi], np.float64).reshape(-1, 2)
+    hmax = max(stats.checks_by_level) if stats.checks_by_level else 0
+    out[f"{prefix}_checks"] = np.array([stats.checks_by_level.get(h, 0) for h in range(hmax + 1)], np.int64)
+    k = stats.kernel
+    out[f"{prefix}_counters"] = np.array([k.iterative_invocations, k.comparison_invocations,
+                                          k.fallback_invocations], np.int64)
+    out[f"{prefix}_single_source"] = np.array([c.source for c in single], np.int64).reshape(-1, 2)
+    print(prefix, "contacts", len(multi), "single", len(single), "checks", out[f"{prefix}_checks"].tolist(),
+          flush=True)
+
+
+def run() -> dict:
+    from tricontact.geometry import RigidMotion
+    from tricontact.kernels import KernelParams
+    from tricontact.scenes import SceneSpec, build_scene
+    from tricontact.stepping import system_from_scene
+
+    out = {}
+    rng = np.random.default_rng(20261020)
+    for count, poses in ((80, 4), (320, 3)):
+        spec = SceneSpec(kind="ParticleParticle", triangle_count=count, initial_gap=1e-3, approach_speed=0.5,
+                         seed=3, relative_tilt_deg=10.0)
+        system = system_from_scene(build_scene(spec), KernelParams())
+        _scene_out(f"s{count}_rest", system, out)
+        rest = system.particles[1].motion.translation.copy()
+        for k in range(poses):
+            # random orientation of particle j at a slightly perturbed rest offset
+            system.particles[1].motion = RigidMotion.random_rotation(
+                rng, translation=rest * (1.0 + rng.uniform(-2e-2, 5e-3)))
+            _scene_out(f"s{count}_p{k}", system, out)
+    spec = SceneSpec(kind="ParticleOnPlane", triangle_count=80, drop_height=0.0)
+    _scene_out("plane", system_from_scene(build_scene(spec), KernelParams()), out)
+    out["scenes"] = np.array(sorted({k.split("_")[0] + "_" + k.split("_")[1] if not k.startswith("plane") else "plane"
+                                     for k in out if k.endswith("_checks")}))
+    return out
+
+
+def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--worker":
+        sys.path.insert(0, str(REF_SRC))
+        np.savez_compressed(sys.argv[2], **run())
+        return
+    for real in ("float64", "float32"):
+        env = dict(os.environ, TRICONTACT_REAL=real, PYTHONPATH=str(REF_SRC))
+        dst = HERE / f"ms_{real}.npz"
+        subprocess.run([sys.executable, __file__, "--worker", str(dst)], env=env, check=True)
+        print("wrote", dst, dst.stat().st_size, "bytes")
+
+
+if __name__ == "__main__":
+    main()
