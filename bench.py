@@ -448,8 +448,78 @@ def configs_table(D, torch, dev):
                     "fallback_rate": s["fallback"] / (1 << 20), "degenerate": s["degenerate"],
                     "contacts": s["contacts"]}
     res["cfg3_fast"] = c3
+    res["multiscale"] = multiscale_table(D, torch, dev)
     res["note"] = ("oracle agreement of cfg2/cfg3: tests/test_gpu_blocks.py, tests/test_gpu_cfg3.py "
                    "(strict bitwise, fast within tolerance with the tie classifier)")
+    return res
+
+
+def multiscale_scene(n_pairs=1024, seed=5):
+    """Particle pairs for the device multiscale traversal: the reference's own
+    320-triangle two-sphere scenes and surrogate trees (tests/golden/ms_float64.npz,
+    produced by the reference), each pair re-posed by a random rigid motion."""
+    from paper_2105_12415_b200 import multiscale as MS
+    from paper_2105_12415_b200.workloads import rotation_matrices
+    g = np.load(ROOT / "tests" / "golden" / "ms_float64.npz")
+    names = [str(s) for s in g["scenes"] if str(s).startswith("s320")]
+    rng = np.random.default_rng(seed)
+    trees = []
+    for k in range(n_pairs):
+        sc = names[k % len(names)]
+        q = rng.normal(size=4)
+        R = rotation_matrices(q[None] / np.linalg.norm(q))[0]
+        shift = rng.uniform(-50, 50, 3)
+        for side in ("i", "j"):
+            x = g[f"{sc}_{side}_tris"].reshape(-1, 3) @ R.T + shift
+            trees.append(MS.FlatTreeArrays(x.reshape(-1, 3, 3), g[f"{sc}_{side}_eps"], g[f"{sc}_{side}_child_off"],
+                                           g[f"{sc}_{side}_child_ids"], g[f"{sc}_{side}_height"],
+                                           int(g[f"{sc}_{side}_n_nodes"])))
+    return trees, np.arange(2 * n_pairs).reshape(-1, 2)
+
+
+def multiscale_table(D, torch, dev, n_pairs=1024):
+    """Device multiscale traversal (8f row 3) vs flat all-pairs detection of the
+    same particle pairs (the blocks kernel on their mesh triangles), reference params."""
+    from paper_2105_12415_b200 import kernels as K, multiscale as MS, particles as PT
+    trees, pairs = multiscale_scene(n_pairs)
+    forest = MS.build_forest(trees, device=dev)
+    kp = K.KernelParams()
+    res = {"particle_pairs": n_pairs}
+    for strict in (False, True):
+        MS.multiscale_contacts(forest, pairs, kp, strict=strict)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = MS.multiscale_contacts(forest, pairs, kp, strict=strict)
+        dt = time.perf_counter() - t0
+        res[f"multiscale_{'strict' if strict else 'fast'}"] = {
+            "ms": dt * 1e3, "call_ms": r.call_ms, "particle_pairs_per_s": n_pairs / dt,
+            "checks": int(r.checks.sum()), "checks_per_s_in_call": int(r.checks.sum()) / (r.call_ms / 1e3),
+            "checks_by_height": r.checks.tolist(), "contacts": r.n_contacts, "fallback": r.stats["fallback"]}
+    # flat detection of the same pairs: every mesh triangle pair through the blocks kernel
+    meshes = np.stack([t.tris[t.n_nodes:] for t in trees])
+    tm = torch.from_numpy(np.ascontiguousarray(meshes)).to(dev)
+    tb = torch.from_numpy(pairs.astype(np.int32)).to(dev)
+    P = D.Params(epsilon=kp.epsilon, n_iterative=kp.n_iterative)
+    PT.blocks_hybrid(tm, tb, P)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = PT.blocks_hybrid(tm, tb, P)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    res["flat_fast"] = {"ms": dt * 1e3, "particle_pairs_per_s": n_pairs / dt,
+                        "checks": n_pairs * meshes.shape[1] ** 2, "contacts": int(out["n_contacts"].item())}
+    # the CPU oracle port of the reference's per-pair traversal, one thread, 16 pairs
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle
+    import ms_oracle
+    sample = [dict(tris=t.tris, eps=t.eps, child_off=t.child_off, child_ids=t.child_ids, height=t.height,
+                   n_nodes=t.n_nodes) for t in trees[:32]]
+    t0 = time.perf_counter()
+    ms_oracle.multiscale(sample, np.arange(32).reshape(-1, 2), oracle.make_params())
+    res["cpu_oracle"] = {"particle_pairs_per_s": 16 / (time.perf_counter() - t0), "cores": 1,
+                         "sample": "16 particle pairs, oracle/ms_oracle.py over the C oracle"}
+    res["note"] = ("wall-clock per call (synchronous host-driven rounds); contacts of multiscale and flat agree "
+                   "(the reference's equivalence lemma)")
     return res
 
 

@@ -1113,16 +1113,30 @@ static int run_multiscale(const T* tris, const T* node_eps, const int32_t* child
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
     // device scratch: frontier (two generations), kind, counts/offsets, tallies
+    // stream-ordered allocations from the device's default pool, kept cached
+    // between calls (release threshold raised once) so a call costs no
+    // cudaMalloc/cudaFree synchronisation
+    static std::once_flag pool_once;
+    std::call_once(pool_once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
     struct Buf {
         void* p = nullptr;
-        ~Buf() { if (p) cudaFree(p); }
+        cudaStream_t s = nullptr;
+        ~Buf() { if (p) cudaFreeAsync(p, s); }
     };
     Buf fr_cur, kbuf, cbuf, obuf, tallies, scan_tmp;
     int64_t cap = n_pairs > 1024 ? n_pairs : 1024;
     auto alloc = [&](Buf& b, size_t bytes) -> cudaError_t {
-        if (b.p) cudaFree(b.p);
+        if (b.p) cudaFreeAsync(b.p, s);
         b.p = nullptr;
-        return cudaMalloc(&b.p, bytes);
+        b.s = s;
+        return cudaMallocAsync(&b.p, bytes, s);
     };
     auto grow = [&](int64_t need) -> cudaError_t {
         cudaError_t r = cudaSuccess;
@@ -1201,22 +1215,28 @@ static int run_multiscale(const T* tris, const T* node_eps, const int32_t* child
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err("multiscale round", e);
         if (total > 0) {
             Buf next;
-            if ((e = cudaMalloc(&next.p, 3 * sizeof(int32_t) * total)) != cudaSuccess) return set_err("cudaMalloc", e);
+            next.s = s;
+            if ((e = cudaMallocAsync(&next.p, 3 * sizeof(int32_t) * total, s)) != cudaSuccess)
+                return set_err("cudaMallocAsync", e);
             int32_t* na = static_cast<int32_t*>(next.p);
             frontier_write_kernel<<<g, 256, 0, s>>>(fa, fb, ftag, n, cnt, off, is_fine, child_off, child_ids, na,
                                                     na + total, na + 2 * total);
             g_launches++;
-            if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err("multiscale unfold", e);
             std::swap(fr_cur.p, next.p);
         }
         n = total;
     }
-    unsigned long long h_nc = 0, h_checks[32];
-    tc_stats h_stats;
-    cudaMemcpy(&h_nc, d_nc, sizeof(h_nc), cudaMemcpyDeviceToHost);
-    cudaMemcpy(h_checks, d_checks, sizeof(h_checks), cudaMemcpyDeviceToHost);
-    cudaMemcpy(&h_stats, d_stats, sizeof(h_stats), cudaMemcpyDeviceToHost);
+    struct {
+        unsigned long long nc, checks[32];
+        tc_stats st;
+    } h;
+    static_assert(sizeof(h) == sizeof(unsigned long long) * 33 + sizeof(tc_stats), "tally layout");
+    cudaMemcpyAsync(&h, tallies.p, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return set_err("multiscale", e);
     if ((e = cudaGetLastError()) != cudaSuccess) return set_err("multiscale", e);
+    const unsigned long long h_nc = h.nc;
+    const unsigned long long* h_checks = h.checks;
+    const tc_stats& h_stats = h.st;
     *n_contacts_host = (int64_t)h_nc;
     if (checks_host)
         for (int k = 0; k <= max_height; ++k) checks_host[k] += (int64_t)h_checks[k];

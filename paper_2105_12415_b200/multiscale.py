@@ -17,6 +17,7 @@ builds them from a reference ``FlatTree`` when one is at hand.
 from __future__ import annotations
 
 import ctypes
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -104,6 +105,7 @@ class MultiscaleResult:
     point_b: np.ndarray
     checks: np.ndarray      # (max_height + 1,) pairings per max height
     stats: dict
+    call_ms: float = 0.0    # wall time of the library call (synchronous)
 
 
 def multiscale_contacts(forest: Forest, pairs, params, *, strict=True, max_contacts=1 << 20,
@@ -125,10 +127,12 @@ def multiscale_contacts(forest: Forest, pairs, params, *, strict=True, max_conta
     p = _abi.params_struct(params, _abi.TC_STRICT if strict else 0)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     fn = getattr(_abi.load(), f"tc_multiscale_{_DT[dt]}")
+    t0 = time.perf_counter()
     rc = fn(_p(forest.tris), _p(forest.eps), _p(forest.child_off), _p(forest.child_ids), _p(forest.is_fine),
             _p(forest.height), int(forest.max_height), roots.ctypes.data, int(roots.shape[0]), ctypes.byref(p),
             int(max_contacts), _p(idx), _p(pa), _p(pb), ctypes.byref(n_contacts), checks.ctypes.data,
             ctypes.byref(st), ctypes.c_void_p(s.cuda_stream))
+    call_ms = (time.perf_counter() - t0) * 1e3
     _abi.check(rc, "tc_multiscale")
     n = int(n_contacts.value)
     m = min(n, max_contacts)
@@ -137,7 +141,7 @@ def multiscale_contacts(forest: Forest, pairs, params, *, strict=True, max_conta
     stats = {k: getattr(st, k) for k in ("iterative", "comparison", "fallback", "degenerate", "contacts",
                                          "intersecting", "min_distance")}
     return MultiscaleResult(n, ih[order, 0], ih[order, 1], ih[order, 2], pa[:m].cpu().numpy()[order],
-                            pb[:m].cpu().numpy()[order], checks, stats)
+                            pb[:m].cpu().numpy()[order], checks, stats, call_ms)
 
 
 def contact_points(forest: Forest, res: MultiscaleResult, pairs):
