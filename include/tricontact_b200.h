@@ -144,19 +144,25 @@ int tc_degenerate_mask_f32(const float* tris, int64_t n, uint8_t* mask, void* st
  * blocks: [n_blocks][2] int32 mesh indices; every block runs the hybrid kernel
  * on all tris_per_mesh^2 triangle pairs (mesh A's triangle i, mesh B's j),
  * both meshes staged in shared memory -- the all-pairs meshgrid of
- * RK/stepping.py:285-308 / RK/contact.py:97-140.  block_eps: per-block halo
+ * RK/stepping.py:285-308 / RK/contact.py:97-140.  mesh_tris: [n_meshes]
+ * triangle count of each mesh (ragged meshes, each <= tris_per_mesh, padded
+ * to that stride), NULL = all tris_per_mesh; a block (m, m) of a mesh
+ * against itself skips the diagonal i == j (RK/contact.py:119-124), so it
+ * runs n (n - 1) pairs.  block_eps: per-block halo
  * (NULL = p->epsilon).  CONTACT pairs are appended (unordered) to
  * contact_idx [max][3] = (block, tri_a, tri_b), contact_distance [max],
  * contact_point_a/b [max][3]; *n_contacts (device int64, caller-zeroed) counts
  * all contacts, also those beyond max_contacts.  tc_stats tallies every pair.
  * Degenerate fallback pairs are counted in stats->degenerate, never listed. */
 int tc_blocks_hybrid_f64(const double* meshes, int32_t tris_per_mesh, int64_t n_meshes,
+                         const int32_t* mesh_tris,
                          const double* motions, const int32_t* blocks, int64_t n_blocks, const double* block_eps,
                          const tc_params* p, int64_t max_contacts, int32_t* contact_idx,
                          double* contact_distance, double* contact_point_a,
                          double* contact_point_b, int64_t* n_contacts, tc_stats* stats,
                          void* stream);
 int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_meshes,
+                         const int32_t* mesh_tris,
                          const float* motions, const int32_t* blocks, int64_t n_blocks, const float* block_eps,
                          const tc_params* p, int64_t max_contacts, int32_t* contact_idx,
                          float* contact_distance, float* contact_point_a,

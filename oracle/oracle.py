@@ -79,7 +79,9 @@ def lib():
             getattr(_lib, f"tco_closest_point_triangle_{sfx}").argtypes = [p, p, i64, p, p, i32]
             getattr(_lib, f"tco_degenerate_{sfx}").argtypes = [p, i64, p, i32]
             getattr(_lib, f"tco_margins_{sfx}").argtypes = [p, p, i64, p, p, p, i32]
-            for name in ("comparison", "iterative", "hybrid", "closest_point_triangle", "degenerate", "margins"):
+            getattr(_lib, f"tco_apply_motion_{sfx}").argtypes = [p, i64, p, p, p]
+            for name in ("comparison", "iterative", "hybrid", "closest_point_triangle", "degenerate", "margins",
+                         "apply_motion"):
                 getattr(_lib, f"tco_{name}_{sfx}").restype = ctypes.c_int
     return _lib
 
@@ -194,6 +196,17 @@ def degenerate(T, dtype=np.float64, threads=1):
     rc = getattr(lib(), f"tco_degenerate_{_sfx(dtype)}")(_ptr(T), T.shape[0], _ptr(m), threads)
     assert rc == 0
     return m.astype(bool)
+
+
+def apply_motion(points, quat, t, dtype=np.float64):
+    """RK/geometry.py:173-176 RigidMotion.apply_points (see tc_oracle_impl.h)."""
+    P = np.ascontiguousarray(points, dtype=dtype).reshape(-1, 3)
+    out = np.empty_like(P)
+    q = np.ascontiguousarray(quat, np.float64).reshape(4)
+    tt = np.ascontiguousarray(t, dtype).reshape(3)
+    rc = getattr(lib(), f"tco_apply_motion_{_sfx(dtype)}")(_ptr(P), P.shape[0], _ptr(q), _ptr(tt), _ptr(out))
+    assert rc == 0
+    return out.reshape(np.shape(points))
 
 
 def margins(A, B, params, eps, dtype=np.float64, threads=1):

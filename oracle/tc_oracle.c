@@ -63,19 +63,23 @@ static void tco_parallel_for(int64_t n, int threads, tco_body_fn fn, void* arg) 
 #define REAL double
 #define SFX f64
 #define SQRT sqrt
+#define FMA fma
 #define DOT3_ORDER_02_1 1
 #include "tc_oracle_impl.h"
 #undef REAL
 #undef SFX
 #undef SQRT
+#undef FMA
 #undef DOT3_ORDER_02_1
 
 #define REAL float
 #define SFX f32
 #define SQRT sqrtf
+#define FMA fmaf
 #define DOT3_ORDER_02_1 0
 #include "tc_oracle_impl.h"
 #undef REAL
 #undef SFX
 #undef SQRT
+#undef FMA
 #undef DOT3_ORDER_02_1

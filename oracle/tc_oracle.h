@@ -46,6 +46,8 @@ typedef struct {
     int tco_closest_point_triangle_##SFX(const REAL* P, const REAL* T, int64_t n,        \
                                          REAL* closest, REAL* bary, int threads);        \
     int tco_degenerate_##SFX(const REAL* T, int64_t n, uint8_t* mask, int threads);              \
+    int tco_apply_motion_##SFX(const REAL* points, int64_t n, const double* quat, const REAL* t, \
+                               REAL* out);                                                    \
     int tco_margins_##SFX(const REAL* A, const REAL* B, int64_t n, const REAL* eps,              \
                           const tco_params* p, double* margins, int threads);
 

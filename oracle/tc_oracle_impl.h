@@ -742,5 +742,28 @@ int FN(tco_degenerate_)(const REAL* T, int64_t n, uint8_t* mask, int threads) {
     return 0;
 }
 
+/* RK/geometry.py:162-176 RigidMotion.apply_points: points @ R.T + t with R
+ * the quaternion's matrix in Python floats rounded to REAL.  NumPy's matmul
+ * of (n, 3) x (3, 3) (OpenBLAS in the reference's environment, checked by
+ * tests/test_motion_oracle.py) evaluates each row as the FMA chain
+ * fma(R_i2, p2, fma(R_i1, p1, R_i0 p0)); the translation is a separate add. */
+int FN(tco_apply_motion_)(const REAL* P, int64_t n, const double* q, const REAL* t, REAL* out) {
+    if (n < 0 || (n > 0 && (!P || !q || !t || !out))) return 1;
+    const double w = q[0], x = q[1], y = q[2], z = q[3];
+    const double m[9] = {1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+                         2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x),
+                         2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)};
+    REAL R[9];
+    for (int k = 0; k < 9; ++k) R[k] = (REAL)m[k];
+    for (int64_t k = 0; k < n; ++k) {
+        const REAL* p = P + 3 * k;
+        for (int i = 0; i < 3; ++i) {
+            const REAL prod = R[3 * i] * p[0];
+            out[3 * k + i] = FMA(R[3 * i + 2], p[2], FMA(R[3 * i + 1], p[1], prod)) + t[i];
+        }
+    }
+    return 0;
+}
+
 #undef TC_TINY_
 #undef FN

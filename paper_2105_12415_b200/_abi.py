@@ -79,9 +79,9 @@ for _s in ("f64", "f32"):
     SIGNATURES[f"tc_hybrid_{_s}"] = (_INT, [_P, _P, _I64, _P, _P, _P] + [_P] * 7 + [_P, _P])
 
 for _s in ("f64", "f32"):
-    # meshes, tris, n_meshes, motions, blocks, n_blocks, block_eps, p, max_contacts, idx, dist, pa, pb,
+    # meshes, tris, n_meshes, mesh_tris, motions, blocks, n_blocks, block_eps, p, max_contacts, idx, dist, pa, pb,
     # n_contacts, stats, stream
-    SIGNATURES[f"tc_blocks_hybrid_{_s}"] = (_INT, [_P, ctypes.c_int32, _I64, _P, _P, _I64, _P, _P, _I64] + [_P] * 7)
+    SIGNATURES[f"tc_blocks_hybrid_{_s}"] = (_INT, [_P, ctypes.c_int32, _I64, _P, _P, _P, _I64, _P, _P, _I64] + [_P] * 7)
 
 for _s in ("f64", "f32"):
     # tris, node_eps, child_off, child_ids, is_fine, height, max_height, roots, n_pairs, p, max_contacts,

@@ -584,8 +584,9 @@ template <typename T>
 struct BlockArgs {
     const T* meshes;          // [n_meshes][tris][9]: world coordinates, or local ones with motions
     const T* motions;         // [n_meshes][7] (qw, qx, qy, qz, tx, ty, tz) or NULL
-    int tris;
+    int tris;                 // staging stride (the largest mesh)
     int64_t n_meshes;
+    const int32_t* mesh_tris; // [n_meshes] triangles per mesh, or NULL (all `tris`)
     const int32_t* blocks;    // [nb][2] mesh indices (A, B)
     int64_t nb;
     const T* block_eps;       // [nb] or NULL
@@ -621,11 +622,13 @@ __device__ __forceinline__ void motion_matrix(const T* m, R* Rm, R* tr) {
     for (int k = 0; k < 3; ++k) tr[k] = R(m[4 + k]);
 }
 
-// world = R p + t, row by row: ((R_i0 p0 + R_i1 p1) + R_i2 p2) + t_i
+// world = p @ R.T + t (RK/geometry.py:173-176) rounded like the reference's
+// NumPy matmul: each row the FMA chain fma(R_i2, p2, fma(R_i1, p1, R_i0 p0)),
+// then the translation (oracle tco_apply_motion_*, pinned to NumPy)
 template <class R>
 __device__ __forceinline__ void apply_motion(const R* Rm, const R* tr, const R* p, R* w) {
 #pragma unroll
-    for (int i = 0; i < 3; ++i) w[i] = ((Rm[3 * i] * p[0] + Rm[3 * i + 1] * p[1]) + Rm[3 * i + 2] * p[2]) + tr[i];
+    for (int i = 0; i < 3; ++i) w[i] = fmav(Rm[3 * i + 2], p[2], fmav(Rm[3 * i + 1], p[1], Rm[3 * i] * p[0])) + tr[i];
 }
 
 template <class R, typename T>
@@ -633,12 +636,13 @@ struct BlockSource {
     const BlockArgs<T>& a;
     const T* mA;
     const T* mB;
-    int tris;
+    int tris;                 // staging stride
+    int cols;                 // triangles of mesh B: pair p = i * cols + k
     int64_t blk;
     R eps;
     __device__ __forceinline__ bool want_ids() const { return false; }
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& e) const {
-        const int i = (int)(j / tris), k = (int)(j % tris);
+        const int i = (int)(j / cols), k = (int)(j % cols);
         A.p = mA + i;
         A.stride = tris;
         B.p = mB + k;
@@ -650,8 +654,8 @@ struct BlockSource {
         const unsigned long long slot = atomicAdd(a.n_contacts, 1ull);
         if ((long long)slot >= a.max_contacts) return;  // counted, not stored
         a.c_idx[3 * slot] = (int32_t)blk;
-        a.c_idx[3 * slot + 1] = (int32_t)(j / tris);
-        a.c_idx[3 * slot + 2] = (int32_t)(j % tris);
+        a.c_idx[3 * slot + 1] = (int32_t)(j / cols);
+        a.c_idx[3 * slot + 2] = (int32_t)(j % cols);
         if (a.c_dist) a.c_dist[slot] = val(r.distance);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -672,11 +676,14 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) blocks_hybrid_kernel(Bl
     T* mB = mA + 9 * tris;
     const KP<R> kp = make_kp<R>(a);
     Tally tl;
-    const int64_t P = (int64_t)tris * tris;
-    const int64_t ntile = (P + BLOCK - 1) / BLOCK;
     for (int64_t blk = blockIdx.x; blk < a.nb; blk += gridDim.x) {
         __syncthreads();  // the previous block is fully drained before its meshes are replaced
         const int64_t ia = a.blocks[2 * blk], ib = a.blocks[2 * blk + 1];
+        const int na = a.mesh_tris ? a.mesh_tris[ia] : tris, nbt = a.mesh_tris ? a.mesh_tris[ib] : tris;
+        // a mesh against itself skips the diagonal (RK/contact.py:119-124)
+        const bool self = ia == ib;
+        const int64_t P = (int64_t)na * nbt;
+        const int64_t ntile = (P + BLOCK - 1) / BLOCK;
         const T* gA = a.meshes + ia * tris * 9;
         const T* gB = a.meshes + ib * tris * 9;
         if (a.motions) {
@@ -685,38 +692,38 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) blocks_hybrid_kernel(Bl
             R RA[9], tA[3], RB[9], tB[3];
             motion_matrix(a.motions + 7 * ia, RA, tA);
             motion_matrix(a.motions + 7 * ib, RB, tB);
-            for (int e = threadIdx.x; e < 3 * tris; e += BLOCK) {
+            for (int e = threadIdx.x; e < 3 * max(na, nbt); e += BLOCK) {
                 const int t = e / 3, v = e - 3 * (e / 3);
                 R pa[3], pb[3], wa[3], wb[3];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    pa[c] = R(__ldg(gA + 3 * e + c));
-                    pb[c] = R(__ldg(gB + 3 * e + c));
+                    pa[c] = R(t < na ? __ldg(gA + 3 * e + c) : T(0));
+                    pb[c] = R(t < nbt ? __ldg(gB + 3 * e + c) : T(0));
                 }
                 apply_motion(RA, tA, pa, wa);
                 apply_motion(RB, tB, pb, wb);
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    mA[(3 * v + c) * tris + t] = val(wa[c]);
-                    mB[(3 * v + c) * tris + t] = val(wb[c]);
+                    if (t < na) mA[(3 * v + c) * tris + t] = val(wa[c]);
+                    if (t < nbt) mB[(3 * v + c) * tris + t] = val(wb[c]);
                 }
             }
         } else {
-            for (int e = threadIdx.x; e < 9 * tris; e += BLOCK) {
+            for (int e = threadIdx.x; e < 9 * max(na, nbt); e += BLOCK) {
                 const int t = e / 9, c = e - 9 * (e / 9);
-                mA[c * tris + t] = __ldg(gA + e);
-                mB[c * tris + t] = __ldg(gB + e);
+                if (t < na) mA[c * tris + t] = __ldg(gA + e);
+                if (t < nbt) mB[c * tris + t] = __ldg(gB + e);
             }
         }
         if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
         __syncthreads();
         const R eps = R(a.block_eps ? a.block_eps[blk] : a.eps_scalar);
-        const BlockSource<R, T> src{a, mA, mB, tris, blk, eps};
+        const BlockSource<R, T> src{a, mA, mB, tris, nbt, blk, eps};
         for (int64_t tile = 0; tile < ntile; ++tile) {
             const int64_t p = tile * BLOCK + threadIdx.x;
             bool enq = false;
-            if (p < P) {
-                const int i = (int)(p / tris), k = (int)(p % tris);
+            const int i = (int)(p / nbt), k = (int)(p - (int64_t)i * nbt);
+            if (p < P && !(self && i == k)) {
                 const SmemTri<R> SA{mA + i, tris}, SB{mB + k, tris};
                 R A[9], B[9];
 #pragma unroll
@@ -984,9 +991,10 @@ static int sm_count() {
 
 template <typename K>
 static int64_t grid_for(K kernel, int64_t n, size_t smem = 0) {
-    if (smem > 48 * 1024) {
-        // opt in to > 48 KB of dynamic shared memory (once per kernel is enough,
-        // but the call is cheap and idempotent)
+    if (smem > 16 * 1024) {
+        // opt in to the dynamic shared memory: static + dynamic may pass the
+        // 48 KB default even when the dynamic part alone does not (the call is
+        // cheap and idempotent)
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     int per_sm = 0;
@@ -1059,8 +1067,8 @@ static int run_device(int variant, const T* tri_a, const T* tri_b, int64_t n, co
 }
 
 template <typename T>
-static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const T* motions, const int32_t* blocks,
-                      int64_t nb,
+static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const int32_t* mesh_tris, const T* motions,
+                      const int32_t* blocks, int64_t nb,
                       const T* block_eps, const tc_params* p, int64_t max_contacts, int32_t* c_idx, T* c_dist,
                       T* c_pa, T* c_pb, int64_t* n_contacts, tc_stats* stats, void* stream) {
     if (!params_ok(p) || nb < 0 || tris < 1 || n_meshes < 1 || max_contacts < 0 || !n_contacts ||
@@ -1076,7 +1084,8 @@ static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const T* 
         return TC_EINVAL;
     }
     BlockArgs<T> a;
-    a.meshes = meshes; a.motions = motions; a.tris = tris; a.n_meshes = n_meshes; a.blocks = blocks; a.nb = nb;
+    a.meshes = meshes; a.motions = motions; a.tris = tris; a.n_meshes = n_meshes; a.mesh_tris = mesh_tris;
+    a.blocks = blocks; a.nb = nb;
     a.block_eps = block_eps; a.eps_scalar = (T)p->epsilon; a.max_contacts = max_contacts;
     a.c_idx = c_idx; a.c_dist = c_dist; a.c_pa = c_pa; a.c_pb = c_pb;
     a.n_contacts = reinterpret_cast<unsigned long long*>(n_contacts);
@@ -1538,21 +1547,23 @@ int tc_degenerate_mask_host_f32(const float* tris, int64_t n, uint8_t* mask) {
     return tc::run_degenerate_host<float>(tris, n, mask);
 }
 
-int tc_blocks_hybrid_f64(const double* meshes, int32_t tris_per_mesh, int64_t n_meshes, const double* motions,
+int tc_blocks_hybrid_f64(const double* meshes, int32_t tris_per_mesh, int64_t n_meshes,
+                         const int32_t* mesh_tris, const double* motions,
                          const int32_t* blocks,
                          int64_t n_blocks, const double* block_eps, const tc_params* p, int64_t max_contacts,
                          int32_t* contact_idx, double* contact_distance, double* contact_point_a,
                          double* contact_point_b, int64_t* n_contacts, tc_stats* stats, void* stream) {
-    return tc::run_blocks<double>(meshes, tris_per_mesh, n_meshes, motions, blocks, n_blocks, block_eps, p, max_contacts,
+    return tc::run_blocks<double>(meshes, tris_per_mesh, n_meshes, mesh_tris, motions, blocks, n_blocks, block_eps, p, max_contacts,
                                   contact_idx, contact_distance, contact_point_a, contact_point_b, n_contacts,
                                   stats, stream);
 }
-int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_meshes, const float* motions,
+int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_meshes,
+                         const int32_t* mesh_tris, const float* motions,
                          const int32_t* blocks,
                          int64_t n_blocks, const float* block_eps, const tc_params* p, int64_t max_contacts,
                          int32_t* contact_idx, float* contact_distance, float* contact_point_a,
                          float* contact_point_b, int64_t* n_contacts, tc_stats* stats, void* stream) {
-    return tc::run_blocks<float>(meshes, tris_per_mesh, n_meshes, motions, blocks, n_blocks, block_eps, p, max_contacts,
+    return tc::run_blocks<float>(meshes, tris_per_mesh, n_meshes, mesh_tris, motions, blocks, n_blocks, block_eps, p, max_contacts,
                                  contact_idx, contact_distance, contact_point_a, contact_point_b, n_contacts, stats,
                                  stream);
 }

@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _abi
+from .contact import contact_from_segment_batch
 
 
 @dataclass
@@ -150,20 +151,13 @@ def contact_points(forest: Forest, res: MultiscaleResult, pairs):
     pair (n, 2) particle ids, source (n, 2) mesh triangle indices, position,
     normal (n, 3), eps (n, 2)."""
     pairs = np.asarray(pairs, np.int64).reshape(-1, 2)
-    real = res.point_a.dtype
     owner = np.searchsorted(forest.base, np.concatenate([res.id_i, res.id_j]), side="right") - 1
     oi, oj = owner[: res.id_i.size], owner[res.id_i.size:]
     src_i = res.id_i - forest.base[oi] - forest.n_nodes[oi]
     src_j = res.id_j - forest.base[oj] - forest.n_nodes[oj]
     eps_a = forest.host_eps[res.id_i].astype(np.float64)
     eps_b = forest.host_eps[res.id_j].astype(np.float64)
-    # the reference's w is a Python float; NumPy 2 casts it to the array type
-    w = (eps_a / (eps_a + eps_b)).astype(real)
-    pa, pb = res.point_a, res.point_b
-    position = pa + w[:, None] * (pb - pa)
-    normal = pa - position
-    small = np.array([np.linalg.norm(v) < 1e-12 for v in normal], bool)
-    normal[small] = 0.0
+    position, normal = contact_from_segment_batch(res.point_a, res.point_b, eps_a, eps_b)
     order = np.lexsort((src_j, src_i, pairs[res.pair, 1], pairs[res.pair, 0]))
     return dict(pair=pairs[res.pair][order], source=np.stack([src_i, src_j], 1)[order], position=position[order],
                 normal=normal[order], eps=np.stack([eps_a, eps_b], 1)[order])

@@ -97,26 +97,6 @@ def cfg2_scene(grid=(16, 16, 8), level: int = 2, seed: int = 2, jitter: float = 
     return np.ascontiguousarray(meshes), pairs[keep].astype(np.int32), gaps[keep]
 
 
-def rotation_matrix_ref(q):
-    """RK/geometry.py:162-171 for one unit quaternion, in Python floats."""
-    w, x, y, z = (float(c) for c in q)
-    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
-                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
-                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
-
-
-def apply_motion_ref(local: np.ndarray, motion: np.ndarray) -> np.ndarray:
-    """World coordinates in the kernel's fused-transform order,
-    ((R_i0 p0 + R_i1 p1) + R_i2 p2) + t_i (elementwise, no FMA)."""
-    R = rotation_matrix_ref(motion[:4]).astype(local.dtype)
-    t = np.asarray(motion[4:7], local.dtype)
-    p = local.reshape(-1, 3)
-    w = np.empty_like(p)
-    for i in range(3):
-        w[:, i] = ((R[i, 0] * p[:, 0] + R[i, 1] * p[:, 1]) + R[i, 2] * p[:, 2]) + t[i]
-    return w.reshape(local.shape)
-
-
 def cfg2_scene_local(**kw):
     """cfg2 as local-space meshes + rigid motions (N, 7): each particle's
     jittered mesh centred at the origin, rotated and translated by its motion."""
@@ -146,13 +126,15 @@ def block_pairs(meshes: np.ndarray, blocks: np.ndarray, which):
     return np.concatenate(As), np.concatenate(Bs)
 
 
-def blocks_hybrid(meshes, blocks, params, *, motions=None, block_eps=None, strict=False, max_contacts=1 << 20,
-                  stats=None, stream=None):
+def blocks_hybrid(meshes, blocks, params, *, motions=None, block_eps=None, mesh_tris=None, strict=False,
+                  max_contacts=1 << 20, stats=None, stream=None):
     """Hybrid kernel over every triangle pair of every block (device tensors).
 
     ``meshes``: (N, T, 3, 3) CUDA tensor (world space, or local space with
     ``motions`` (N, 7) = quaternion (w, x, y, z) + translation, applied while
-    the meshes are staged); ``blocks``: (nb, 2) int32 CUDA tensor.
+    the meshes are staged); ``blocks``: (nb, 2) int32 CUDA tensor;
+    ``mesh_tris``: (N,) triangles per mesh for ragged meshes padded to T.
+    A block (m, m) skips the diagonal (a triangle is never tested against itself).
     Returns a dict: n_contacts (device int64 scalar tensor) and the contact
     arrays idx (max, 3) int32 [block, tri_a, tri_b], distance, point_a, point_b
     (unordered; ``sort_contacts`` orders them like the reference).
@@ -177,8 +159,11 @@ def blocks_hybrid(meshes, blocks, params, *, motions=None, block_eps=None, stric
         block_eps = block_eps.to(device=dev, dtype=dt).contiguous()
     if motions is not None:
         motions = motions.to(device=dev, dtype=dt).contiguous()
+    if mesh_tris is not None:
+        mesh_tris = torch.as_tensor(mesh_tris, dtype=torch.int32).to(dev).contiguous()
     fn = getattr(_abi.load(), f"tc_blocks_hybrid_{_DT[dt]}")
-    rc = fn(_p(meshes), int(meshes.shape[1]), int(meshes.shape[0]), _p(motions), _p(blocks), int(blocks.shape[0]),
+    rc = fn(_p(meshes), int(meshes.shape[1]), int(meshes.shape[0]), _p(mesh_tris), _p(motions), _p(blocks),
+            int(blocks.shape[0]),
             _p(block_eps), ctypes.byref(p), int(max_contacts), _p(out["idx"]), _p(out["distance"]),
             _p(out["point_a"]), _p(out["point_b"]), _p(out["n_contacts"]), _p(stats),
             ctypes.c_void_p(st.cuda_stream))

@@ -34,7 +34,10 @@ def _flat_arrays(particle, motion):
     child_off[1:] = np.cumsum([c.size for c in f.children])
     child_ids = np.concatenate([c for c in f.children if c.size]).astype(np.int32)
     return dict(tris=particle.world_tris(motion).reshape(-1, 9), eps=f.eps.copy(), child_off=child_off,
-                child_ids=child_ids, height=f.height.astype(np.int32), n_nodes=np.int64(f.n_nodes))
+                child_ids=child_ids, height=f.height.astype(np.int32), n_nodes=np.int64(f.n_nodes),
+                local=f.tri.reshape(-1, 9).copy(),
+                motion=np.concatenate([np.asarray(motion.rotation, np.float64),
+                                       np.asarray(motion.translation, np.float64)]))
 
 
 def _scene_out(prefix, system, out):
@@ -59,8 +62,54 @@ def _scene_out(prefix, system, out):
     out[f"{prefix}_counters"] = np.array([k.iterative_invocations, k.comparison_invocations,
                                           k.fallback_invocations], np.int64)
     out[f"{prefix}_single_source"] = np.array([c.source for c in single], np.int64).reshape(-1, 2)
+    out[f"{prefix}_single_position"] = np.array([c.position for c in single]).reshape(-1, 3)
+    out[f"{prefix}_single_normal"] = np.array([c.normal for c in single]).reshape(-1, 3)
+    out[f"{prefix}_single_eps"] = np.array([pi.epsilon, pj.epsilon], np.float64)
     print(prefix, "contacts", len(multi), "single", len(single), "checks", out[f"{prefix}_checks"].tolist(),
           flush=True)
+
+
+def _find_contacts_cases(out):
+    """RK/contact.py:97-140 find_contacts_single_level: two soups with unequal
+    halos, a soup against itself (diagonal skipped), ragged sizes."""
+    from tricontact.contact import find_contacts_single_level
+    from tricontact.geometry import flatten
+    from tricontact.kernels import KernelCounters, KernelParams
+    from tricontact.scenes import SceneSpec, build_scene
+    from tricontact.stepping import system_from_scene
+
+    spec = SceneSpec(kind="ParticleParticle", triangle_count=80, initial_gap=1e-3, approach_speed=0.5,
+                     seed=3, relative_tilt_deg=10.0)
+    sysm = system_from_scene(build_scene(spec), KernelParams())
+    wi = sysm.particles[0].world_tris().reshape(-1, 3, 3)[sysm.particles[0].flat.n_nodes:]
+    wj = sysm.particles[1].world_tris().reshape(-1, 3, 3)[sysm.particles[1].flat.n_nodes:]
+    plane = system_from_scene(build_scene(SceneSpec(kind="ParticleOnPlane", triangle_count=80, drop_height=0.0)),
+                              KernelParams())
+    pl = [p.world_tris().reshape(-1, 3, 3)[p.flat.n_nodes:] for p in plane.particles]
+    soup = flatten(wi)
+    cases = {
+        "two": (flatten(wi), flatten(wj), 1e-2, 2e-2),
+        "self": (soup, soup, None, None),
+        "ragged": (flatten(pl[0]), flatten(pl[1]), None, None),
+        "ragged_t": (flatten(pl[1]), flatten(pl[0]), 5e-3, 1e-2),
+    }
+    names = []
+    for name, (si, sj, ei, ej) in cases.items():
+        counters = KernelCounters()
+        res = find_contacts_single_level(si, sj, KernelParams(), counters, pair=(3, 7), eps_i=ei, eps_j=ej)
+        pre = f"fc_{name}"
+        names.append(name)
+        out[f"{pre}_tris_i"] = si.triangles().reshape(-1, 9).copy()
+        out[f"{pre}_tris_j"] = sj.triangles().reshape(-1, 9).copy()
+        out[f"{pre}_same"] = np.bool_(si is sj)
+        out[f"{pre}_eps"] = np.array([np.nan if ei is None else ei, np.nan if ej is None else ej])
+        out[f"{pre}_source"] = np.array([c.source for c in res], np.int64).reshape(-1, 2)
+        out[f"{pre}_position"] = np.array([c.position for c in res]).reshape(-1, 3)
+        out[f"{pre}_normal"] = np.array([c.normal for c in res]).reshape(-1, 3)
+        out[f"{pre}_counters"] = np.array([counters.iterative_invocations, counters.comparison_invocations,
+                                           counters.fallback_invocations], np.int64)
+        print(pre, "contacts", len(res), flush=True)
+    out["fc_cases"] = np.array(names)
 
 
 def run() -> dict:
@@ -84,6 +133,7 @@ def run() -> dict:
             _scene_out(f"s{count}_p{k}", system, out)
     spec = SceneSpec(kind="ParticleOnPlane", triangle_count=80, drop_height=0.0)
     _scene_out("plane", system_from_scene(build_scene(spec), KernelParams()), out)
+    _find_contacts_cases(out)
     out["scenes"] = np.array(sorted({k.split("_")[0] + "_" + k.split("_")[1] if not k.startswith("plane") else "plane"
                                      for k in out if k.endswith("_checks")}))
     return out

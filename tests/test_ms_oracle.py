@@ -36,3 +36,16 @@ def test_golden_equivalence_lemma(real):
     for sc in scenes(g):
         assert np.array_equal(g[f"{sc}_source"], g[f"{sc}_single_source"]), sc
     assert sum(g[f"{sc}_source"].shape[0] for sc in scenes(g)) > 50
+
+
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_oracle_apply_motion_matches_reference(oracle_lib, real):
+    # RK/geometry.py:173-176 apply_points (the reference's world_tris) == the
+    # oracle's FMA-chain restatement, bitwise, on every golden particle
+    g = load(real)
+    dt = DTYPES[real]
+    for sc in scenes(g):
+        for side in ("i", "j"):
+            m = g[f"{sc}_{side}_motion"]
+            w = oracle_lib.apply_motion(g[f"{sc}_{side}_local"].reshape(-1, 3), m[:4], m[4:].astype(dt), dtype=dt)
+            assert w.tobytes() == g[f"{sc}_{side}_tris"].astype(dt).reshape(-1, 3).tobytes(), (sc, side)
