@@ -173,7 +173,10 @@ int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_m
  * RK/stepping.py:311-368 multiscale_contacts for n_pairs particle pairs at
  * once.  The surrogate trees of all particles are concatenated FlatTree arrays
  * (RK/stepping.py:78-129) under one global id space (DEVICE pointers):
- * tris [n_total][9] world coordinates, node_eps [n_total], child_off
+ * tris [n_total][9] world coordinates -- or local ones when motions
+ * ([n_particles][7], as tc_blocks_hybrid_*) is given, node_owner [n_total]
+ * naming each node's particle: the rigid motion is then applied to every
+ * node as it is loaded (RK/stepping.py:157-159 world_tris) -- node_eps [n_total], child_off
  * [n_total + 1] / child_ids (CSR children, global ids; a leaf node lists its
  * mesh triangles), is_fine [n_total] (1 = mesh triangle), height [n_total]
  * (0 = mesh level).  roots: HOST [n_pairs][2] global root ids (i, j).
@@ -190,13 +193,15 @@ int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_m
  * degenerate triangle (the reference raises DegenerateTriangle).  Params
  * flags: TC_STRICT only.  Synchronous on `stream` (one 8-byte read-back per
  * round). */
-int tc_multiscale_f64(const double* tris, const double* node_eps, const int32_t* child_off,
+int tc_multiscale_f64(const double* tris, const int32_t* node_owner, const double* motions,
+                      const double* node_eps, const int32_t* child_off,
                       const int32_t* child_ids, const uint8_t* is_fine, const int32_t* height,
                       int32_t max_height, const int32_t* roots, int64_t n_pairs, const tc_params* p,
                       int64_t max_contacts, int32_t* contact_idx, double* contact_point_a,
                       double* contact_point_b, int64_t* n_contacts, int64_t* checks, tc_stats* stats,
                       void* stream);
-int tc_multiscale_f32(const float* tris, const float* node_eps, const int32_t* child_off,
+int tc_multiscale_f32(const float* tris, const int32_t* node_owner, const float* motions,
+                      const float* node_eps, const int32_t* child_off,
                       const int32_t* child_ids, const uint8_t* is_fine, const int32_t* height,
                       int32_t max_height, const int32_t* roots, int64_t n_pairs, const tc_params* p,
                       int64_t max_contacts, int32_t* contact_idx, float* contact_point_a,

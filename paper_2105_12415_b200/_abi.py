@@ -84,9 +84,9 @@ for _s in ("f64", "f32"):
     SIGNATURES[f"tc_blocks_hybrid_{_s}"] = (_INT, [_P, ctypes.c_int32, _I64, _P, _P, _P, _I64, _P, _P, _I64] + [_P] * 7)
 
 for _s in ("f64", "f32"):
-    # tris, node_eps, child_off, child_ids, is_fine, height, max_height, roots, n_pairs, p, max_contacts,
-    # idx, pa, pb, n_contacts, checks, stats, stream
-    SIGNATURES[f"tc_multiscale_{_s}"] = (_INT, [_P] * 6 + [ctypes.c_int32, _P, _I64, _P, _I64] + [_P] * 7)
+    # tris, node_owner, motions, node_eps, child_off, child_ids, is_fine, height, max_height, roots, n_pairs, p,
+    # max_contacts, idx, pa, pb, n_contacts, checks, stats, stream
+    SIGNATURES[f"tc_multiscale_{_s}"] = (_INT, [_P] * 8 + [ctypes.c_int32, _P, _I64, _P, _I64] + [_P] * 7)
 
 _lib = None
 

@@ -769,7 +769,9 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) blocks_hybrid_kernel(Bl
 
 template <typename T>
 struct FrontierArgs {
-    const T* tris;            // [n_total][9] world coordinates
+    const T* tris;            // [n_total][9] world coordinates, or local ones with motions
+    const int32_t* owner;     // [n_total] particle of each node (with motions)
+    const T* motions;         // [n_particles][7] (qw, qx, qy, qz, tx, ty, tz) or NULL
     const T* node_eps;        // [n_total]
     const uint8_t* is_fine;   // [n_total]
     const int32_t* height;    // [n_total]
@@ -790,6 +792,26 @@ struct FrontierArgs {
     int n_iterative;
 };
 
+// One tree node's triangle; with motions the owner's rigid motion is applied
+// on the fly (RK/stepping.py:157-159 world_tris, rounded like apply_points).
+template <class R, typename T>
+__device__ __forceinline__ void load_node(const FrontierArgs<T>& a, int64_t id, R* X) {
+    if (a.motions) {
+        R Rm[9], tr[3];
+        motion_matrix(a.motions + 7 * (int64_t)a.owner[id], Rm, tr);
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+            R p[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) p[c] = R(__ldg(a.tris + 9 * id + 3 * v + c));
+            apply_motion(Rm, tr, p, X + 3 * v);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) X[k] = R(__ldg(a.tris + 9 * id + k));
+    }
+}
+
 template <class R, typename T>
 struct FrontierSource {
     const FrontierArgs<T>& a;
@@ -797,10 +819,13 @@ struct FrontierSource {
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
         T* slot = thread_slot<T>(18 * BLOCK);
         const int64_t ia = a.fa[j], ib = a.fb[j];
+        R X[9], Y[9];
+        load_node(a, ia, X);
+        load_node(a, ib, Y);
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-            slot[k * BLOCK] = __ldg(a.tris + 9 * ia + k);
-            slot[(9 + k) * BLOCK] = __ldg(a.tris + 9 * ib + k);
+            slot[k * BLOCK] = val(X[k]);
+            slot[(9 + k) * BLOCK] = val(Y[k]);
         }
         A.p = slot;
         A.stride = BLOCK;
@@ -845,11 +870,8 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) frontier_hybrid_kernel(
         if (i < a.n) {
             const int64_t ia = a.fa[i], ib = a.fb[i];
             R A[9], B[9];
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                A[k] = R(__ldg(a.tris + 9 * ia + k));
-                B[k] = R(__ldg(a.tris + 9 * ib + k));
-            }
+            load_node(a, ia, A);
+            load_node(a, ib, B);
             T* slot = thread_slot<T>(18 * BLOCK);
             stash_pair(slot, A, B);
             const bool both_fine = a.is_fine[ia] && a.is_fine[ib];
@@ -1107,13 +1129,14 @@ static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const int
 // Host driver of the multiscale traversal: one hybrid launch + unfolding per
 // round, until the frontier is empty (one 8-byte read-back per round).
 template <typename T>
-static int run_multiscale(const T* tris, const T* node_eps, const int32_t* child_off, const int32_t* child_ids,
+static int run_multiscale(const T* tris, const int32_t* owner, const T* motions, const T* node_eps,
+                          const int32_t* child_off, const int32_t* child_ids,
                           const uint8_t* is_fine, const int32_t* height, int32_t max_height, const int32_t* roots,
                           int64_t n_pairs, const tc_params* p, int64_t max_contacts, int32_t* c_idx, T* c_pa,
                           T* c_pb, int64_t* n_contacts_host, int64_t* checks_host, tc_stats* stats_host,
                           void* stream) {
     if (!params_ok(p) || n_pairs < 0 || max_height < 0 || max_height > 31 || max_contacts < 0 ||
-        (p->flags & (TC_SOA | TC_EMIT_IDS)) || !n_contacts_host) {
+        (p->flags & (TC_SOA | TC_EMIT_IDS)) || !n_contacts_host || (motions && !owner)) {
         snprintf(g_err, sizeof(g_err), "invalid argument (multiscale)");
         return TC_EINVAL;
     }
@@ -1189,7 +1212,7 @@ static int run_multiscale(const T* tris, const T* node_eps, const int32_t* child
         int32_t* fb = fa + n;
         int32_t* ftag = fb + n;
         FrontierArgs<T> a;
-        a.tris = tris; a.node_eps = node_eps; a.is_fine = is_fine; a.height = height;
+        a.tris = tris; a.owner = owner; a.motions = motions; a.node_eps = node_eps; a.is_fine = is_fine; a.height = height;
         a.fa = fa; a.fb = fb; a.ftag = ftag; a.n = n;
         a.kind = static_cast<int8_t*>(kbuf.p);
         a.max_contacts = max_contacts; a.c_idx = c_idx; a.c_pa = c_pa; a.c_pb = c_pb;
@@ -1568,21 +1591,21 @@ int tc_blocks_hybrid_f32(const float* meshes, int32_t tris_per_mesh, int64_t n_m
                                  stream);
 }
 
-int tc_multiscale_f64(const double* tris, const double* node_eps, const int32_t* child_off, const int32_t* child_ids,
+int tc_multiscale_f64(const double* tris, const int32_t* node_owner, const double* motions, const double* node_eps, const int32_t* child_off, const int32_t* child_ids,
                       const uint8_t* is_fine, const int32_t* height, int32_t max_height, const int32_t* roots,
                       int64_t n_pairs, const tc_params* p, int64_t max_contacts, int32_t* contact_idx,
                       double* contact_point_a, double* contact_point_b, int64_t* n_contacts, int64_t* checks,
                       tc_stats* stats, void* stream) {
-    return tc::run_multiscale<double>(tris, node_eps, child_off, child_ids, is_fine, height, max_height, roots,
+    return tc::run_multiscale<double>(tris, node_owner, motions, node_eps, child_off, child_ids, is_fine, height, max_height, roots,
                                       n_pairs, p, max_contacts, contact_idx, contact_point_a, contact_point_b,
                                       n_contacts, checks, stats, stream);
 }
-int tc_multiscale_f32(const float* tris, const float* node_eps, const int32_t* child_off, const int32_t* child_ids,
+int tc_multiscale_f32(const float* tris, const int32_t* node_owner, const float* motions, const float* node_eps, const int32_t* child_off, const int32_t* child_ids,
                       const uint8_t* is_fine, const int32_t* height, int32_t max_height, const int32_t* roots,
                       int64_t n_pairs, const tc_params* p, int64_t max_contacts, int32_t* contact_idx,
                       float* contact_point_a, float* contact_point_b, int64_t* n_contacts, int64_t* checks,
                       tc_stats* stats, void* stream) {
-    return tc::run_multiscale<float>(tris, node_eps, child_off, child_ids, is_fine, height, max_height, roots,
+    return tc::run_multiscale<float>(tris, node_owner, motions, node_eps, child_off, child_ids, is_fine, height, max_height, roots,
                                      n_pairs, p, max_contacts, contact_idx, contact_point_a, contact_point_b,
                                      n_contacts, checks, stats, stream);
 }

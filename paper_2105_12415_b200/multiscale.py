@@ -30,7 +30,7 @@ from .contact import contact_from_segment_batch
 class FlatTreeArrays:
     """One particle's FlatTree in array form (ids: nodes in preorder, then mesh triangles)."""
 
-    tris: np.ndarray        # (n_total, 3, 3) world coordinates
+    tris: np.ndarray        # (n_total, 3, 3) world coordinates (local ones when the forest has motions)
     eps: np.ndarray         # (n_total,)
     child_off: np.ndarray   # (n_total + 1,) CSR offsets
     child_ids: np.ndarray   # children ids (local)
@@ -65,10 +65,26 @@ class Forest:
     n_nodes: np.ndarray     # (n_particles,)
     max_height: int
     host_eps: np.ndarray = field(repr=False, default=None)
+    owner: object = None    # (n_total,) int32 particle of each node (with motions)
+    motions: object = None  # (n_particles, 7) quaternion (w, x, y, z) + translation, or None
+
+    def set_motions(self, motions) -> None:
+        """Rigid motions of every particle (the trees then hold local coordinates)."""
+        import torch
+        m = torch.as_tensor(np.asarray(motions), dtype=self.tris.dtype).to(self.tris.device).contiguous()
+        if m.shape != (self.base.shape[0], 7):
+            raise ValueError("motions must be (n_particles, 7)")
+        if self.owner is None:
+            sizes = np.diff(np.append(self.base, self.tris.shape[0]))
+            own = np.repeat(np.arange(self.base.shape[0], dtype=np.int32), sizes)
+            self.owner = torch.from_numpy(own).to(self.tris.device)
+        self.motions = m
 
 
-def build_forest(trees: list[FlatTreeArrays], device="cuda", dtype=None) -> Forest:
-    """Concatenate trees into one device-resident global id space."""
+def build_forest(trees: list[FlatTreeArrays], device="cuda", dtype=None, motions=None) -> Forest:
+    """Concatenate trees into one device-resident global id space.  With
+    ``motions`` (n_particles, 7) the trees hold local coordinates and every
+    node is transformed by its particle's motion as the kernel loads it."""
     import torch
 
     dtype = dtype or trees[0].tris.dtype
@@ -91,9 +107,12 @@ def build_forest(trees: list[FlatTreeArrays], device="cuda", dtype=None) -> Fore
     height = np.concatenate([np.asarray(t.height, np.int32) for t in trees])
     tt = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=device)  # noqa: E731
     fdt = torch.float64 if np.dtype(dtype) == np.float64 else torch.float32
-    return Forest(tt(tris, fdt), tt(eps, fdt), tt(child_off, torch.int32), tt(child_ids, torch.int32),
-                  tt(is_fine, torch.uint8), tt(height, torch.int32), base,
-                  np.array([t.n_nodes for t in trees], np.int64), int(height.max()), eps)
+    forest = Forest(tt(tris, fdt), tt(eps, fdt), tt(child_off, torch.int32), tt(child_ids, torch.int32),
+                    tt(is_fine, torch.uint8), tt(height, torch.int32), base,
+                    np.array([t.n_nodes for t in trees], np.int64), int(height.max()), eps)
+    if motions is not None:
+        forest.set_motions(motions)
+    return forest
 
 
 @dataclass
@@ -129,7 +148,7 @@ def multiscale_contacts(forest: Forest, pairs, params, *, strict=True, max_conta
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     fn = getattr(_abi.load(), f"tc_multiscale_{_DT[dt]}")
     t0 = time.perf_counter()
-    rc = fn(_p(forest.tris), _p(forest.eps), _p(forest.child_off), _p(forest.child_ids), _p(forest.is_fine),
+    rc = fn(_p(forest.tris), _p(forest.owner), _p(forest.motions), _p(forest.eps), _p(forest.child_off), _p(forest.child_ids), _p(forest.is_fine),
             _p(forest.height), int(forest.max_height), roots.ctypes.data, int(roots.shape[0]), ctypes.byref(p),
             int(max_contacts), _p(idx), _p(pa), _p(pb), ctypes.byref(n_contacts), checks.ctypes.data,
             ctypes.byref(st), ctypes.c_void_p(s.cuda_stream))

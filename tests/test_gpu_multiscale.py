@@ -110,3 +110,38 @@ def test_capacity_and_empty():
     assert res.n_contacts == 0 and not res.checks.any()
     res, _ = _run(trees, [(0, 1)], np.float64, max_contacts=3)
     assert res.n_contacts == g[f"{sc}_source"].shape[0] and res.pair.size == 3
+
+
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_fused_motion_matches_reference(real):
+    # local node coordinates + per-particle rigid motions, transformed as the
+    # frontier loads them (8f row 2), reproduce the reference's world-space run
+    from paper_2105_12415_b200 import kernels, multiscale as ms
+
+    g = load(real)
+    dt = DTYPES[real]
+    trees, motions, pairs, scs = [], [], [], []
+    for sc in scenes(g):
+        for side in ("i", "j"):
+            t = tree(g, sc, side)
+            trees.append(ms.FlatTreeArrays(g[f"{sc}_{side}_local"].reshape(-1, 3, 3), t["eps"], t["child_off"],
+                                           t["child_ids"], t["height"], t["n_nodes"]))
+            motions.append(g[f"{sc}_{side}_motion"])
+        pairs.append((len(trees) - 2, len(trees) - 1))
+        scs.append(sc)
+    forest = ms.build_forest(trees, dtype=dt, motions=np.stack(motions))
+    for strict in (True, False):
+        res = ms.multiscale_contacts(forest, pairs, kernels.KernelParams(), strict=strict)
+        cp = ms.contact_points(forest, res, pairs)
+        for k, sc in enumerate(scs):
+            sel = cp["pair"][:, 0] == pairs[k][0]
+            if strict:
+                assert np.array_equal(cp["source"][sel], g[f"{sc}_source"]), sc
+                assert cp["position"][sel].tobytes() == g[f"{sc}_position"].astype(dt).tobytes(), sc
+                assert cp["normal"][sel].tobytes() == g[f"{sc}_normal"].astype(dt).tobytes(), sc
+        if not strict:
+            # fused fast == world-space fast, bitwise (the transform rounds like the reference)
+            wt = [tree(g, sc, side) for sc in scs for side in ("i", "j")]
+            res_w, cp_w = _run(wt, pairs, dt, strict=False)
+            assert np.array_equal(cp["source"], cp_w["source"])
+            assert cp["position"].tobytes() == cp_w["position"].tobytes()
