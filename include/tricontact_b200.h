@@ -132,6 +132,19 @@ int tc_closest_point_triangle_f64(const double* points, const double* tris, int6
 int tc_closest_point_triangle_f32(const float* points, const float* tris, int64_t n,
                                   float* closest, float* bary, void* stream);
 
+/* Point-to-triangle distance for the surrogate halo checks
+ * (RK/surrogate.py:237-257 conservative_epsilon, :463-505
+ * validate_conservative): distance[i] = |points[i] - closest point of
+ * tris[tri_index[i]]| (tri_index NULL = tris[i], then n <= n_tris), rounded
+ * like np.linalg.norm(p - closest_point_triangle_batch(p, t)[0], axis=1);
+ * closest (n,3) optional.  Always strict IEEE (bit-identical). */
+int tc_point_triangle_distance_f64(const double* points, const double* tris, int64_t n_tris,
+                                   const int32_t* tri_index, int64_t n, double* distance,
+                                   double* closest, void* stream);
+int tc_point_triangle_distance_f32(const float* points, const float* tris, int64_t n_tris,
+                                   const int32_t* tri_index, int64_t n, float* distance,
+                                   float* closest, void* stream);
+
 /* RK/geometry.py:68 degenerate_mask (rel_tol 1e-12): tris (n,3,3) -> mask (n,). */
 int tc_degenerate_mask_f64(const double* tris, int64_t n, uint8_t* mask, void* stream);
 int tc_degenerate_mask_f32(const float* tris, int64_t n, uint8_t* mask, void* stream);

@@ -61,6 +61,8 @@ SIGNATURES = {
     "tc_fma_probe": (_I64, [_INT, _I64, _INT, _P, _P]),
     "tc_closest_point_triangle_f64": (_INT, [_P, _P, _I64, _P, _P, _P]),
     "tc_closest_point_triangle_f32": (_INT, [_P, _P, _I64, _P, _P, _P]),
+    "tc_point_triangle_distance_f64": (_INT, [_P, _P, _I64, _P, _I64, _P, _P, _P]),
+    "tc_point_triangle_distance_f32": (_INT, [_P, _P, _I64, _P, _I64, _P, _P, _P]),
     "tc_degenerate_mask_f64": (_INT, [_P, _I64, _P, _P]),
     "tc_degenerate_mask_f32": (_INT, [_P, _I64, _P, _P]),
     "tc_closest_point_triangle_host_f64": (_INT, [_P, _P, _I64, _P, _P]),

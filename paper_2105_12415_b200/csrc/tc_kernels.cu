@@ -960,6 +960,29 @@ __global__ void __launch_bounds__(BLOCK) cpt_kernel(const T* P, const T* Tr, int
     }
 }
 
+// Point-to-triangle distance with an indexed triangle per point (surrogate
+// halo checks, RK/surrogate.py:237-257 conservative_epsilon and :463-505
+// validate_conservative): closest point (RK/kernels.py:157), then
+// np.linalg.norm(p - closest) in the reference's order, all in strict IEEE.
+template <typename T>
+__global__ void __launch_bounds__(BLOCK) ptd_kernel(const T* P, const T* Tr, const int32_t* tri_index, int64_t n,
+                                                    T* distance, T* closest) {
+    using R = Strict<T>;
+    for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
+        const int64_t t_i = tri_index ? (int64_t)__ldg(tri_index + i) : i;
+        R p[3], t[9], c[3], u, w, d[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) p[k] = R(__ldg(P + 3 * i + k));
+#pragma unroll
+        for (int k = 0; k < 9; ++k) t[k] = R(__ldg(Tr + 9 * t_i + k));
+        closest_point_triangle(p, t, c, u, w);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) d[k] = p[k] - c[k];
+        distance[i] = sqrtv(norm3_sq_sum(d)).v;
+        if (closest) { closest[3 * i] = c[0].v; closest[3 * i + 1] = c[1].v; closest[3 * i + 2] = c[2].v; }
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(BLOCK) degenerate_kernel(const T* Tr, int64_t n, uint8_t* mask) {
     using R = Strict<T>;
@@ -1420,6 +1443,19 @@ static int run_cpt(const T* P, const T* Tr, int64_t n, T* closest, T* bary, void
 }
 
 template <typename T>
+static int run_ptd(const T* P, const T* Tr, int64_t n_tris, const int32_t* tri_index, int64_t n, T* distance,
+                   T* closest, void* stream) {
+    if (n < 0 || n_tris < 0 || (n > 0 && (!P || !Tr || !distance)) || (!tri_index && n > n_tris)) return TC_EINVAL;
+    if (n == 0) return TC_OK;
+    auto k = ptd_kernel<T>;
+    k<<<(unsigned)grid_for(k, n), BLOCK, 0, reinterpret_cast<cudaStream_t>(stream)>>>(P, Tr, tri_index, n, distance,
+                                                                                       closest);
+    g_launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TC_OK : set_err("point-triangle launch", e);
+}
+
+template <typename T>
 static int run_degenerate(const T* Tr, int64_t n, uint8_t* mask, void* stream) {
     if (n < 0 || (n > 0 && (!Tr || !mask))) return TC_EINVAL;
     if (n == 0) return TC_OK;
@@ -1547,6 +1583,15 @@ int tc_closest_point_triangle_f64(const double* points, const double* tris, int6
 int tc_closest_point_triangle_f32(const float* points, const float* tris, int64_t n, float* closest, float* bary,
                                   void* stream) {
     return tc::run_cpt<float>(points, tris, n, closest, bary, stream);
+}
+int tc_point_triangle_distance_f64(const double* points, const double* tris, int64_t n_tris,
+                                   const int32_t* tri_index, int64_t n, double* distance, double* closest,
+                                   void* stream) {
+    return tc::run_ptd<double>(points, tris, n_tris, tri_index, n, distance, closest, stream);
+}
+int tc_point_triangle_distance_f32(const float* points, const float* tris, int64_t n_tris, const int32_t* tri_index,
+                                   int64_t n, float* distance, float* closest, void* stream) {
+    return tc::run_ptd<float>(points, tris, n_tris, tri_index, n, distance, closest, stream);
 }
 int tc_degenerate_mask_f64(const double* tris, int64_t n, uint8_t* mask, void* stream) {
     return tc::run_degenerate<double>(tris, n, mask, stream);

@@ -112,6 +112,61 @@ def _find_contacts_cases(out):
     out["fc_cases"] = np.array(names)
 
 
+def _tree_arrays(tree, pre, out):
+    nodes = list(tree.nodes())
+    index = {id(n): k for k, n in enumerate(nodes)}
+    out[f"{pre}_node_tri"] = np.stack([np.asarray(n.triangle, np.float64).reshape(3, 3) for n in nodes])
+    out[f"{pre}_node_eps"] = np.array([float(n.epsilon) for n in nodes])
+    out[f"{pre}_node_leaf"] = np.array([n.is_leaf for n in nodes])
+    kids = [np.array([index[id(c)] for c in n.children], np.int64) for n in nodes]
+    leaves = [np.asarray(n.leaf_indices(), np.int64) for n in nodes]
+    for name, lists in (("kids", kids), ("leafidx", leaves)):
+        off = np.zeros(len(nodes) + 1, np.int64)
+        off[1:] = np.cumsum([a.size for a in lists])
+        out[f"{pre}_{name}_off"] = off
+        out[f"{pre}_{name}"] = np.concatenate(lists) if off[-1] else np.zeros(0, np.int64)
+    out[f"{pre}_finest"] = np.float64(tree.finest_epsilon)
+
+
+def _surrogate_cases(out):
+    """RK/surrogate.py:237-257 conservative_epsilon and :463-505
+    validate_conservative on reference-built trees."""
+    from tricontact.geometry import triangle
+    from tricontact.kernels import KernelParams
+    from tricontact.scenes import SceneSpec, build_scene
+    from tricontact.stepping import system_from_scene
+    from tricontact.surrogate import build_surrogate_tree, conservative_epsilon, validate_conservative
+
+    rng = np.random.default_rng(99)
+    for count in (80, 320):
+        spec = SceneSpec(kind="ParticleParticle", triangle_count=count, initial_gap=1e-3, approach_speed=0.5,
+                         seed=3, relative_tilt_deg=10.0)
+        p = system_from_scene(build_scene(spec), KernelParams()).particles[0]
+        mesh = p.body_tris.reshape(-1, 3, 3)
+        tree = build_surrogate_tree(mesh, 8, seed=0)
+        pre = f"sg{count}"
+        out[f"{pre}_mesh"] = mesh.reshape(-1, 9).copy()
+        _tree_arrays(tree, pre, out)
+        for spt in (10, 3):
+            r = validate_conservative(tree, mesh, samples_per_triangle=spt)
+            out[f"{pre}_valid_{spt}"] = np.array([r["worst_slack"], float(r["ok"]), r["checked_nodes"]])
+        tree.root.epsilon *= 0.5
+        r = validate_conservative(tree, mesh)
+        out[f"{pre}_halved_valid"] = np.array([r["worst_slack"], float(r["ok"]), r["checked_nodes"]])
+        print(pre, "nodes", out[f"{pre}_valid_10"], out[f"{pre}_halved_valid"], flush=True)
+    ce = []
+    t = triangle([0, 0, 0], [1, 0, 0], [0, 1, 0])
+    cases = [(t, t[None], 0.25), (t, (t + np.array([0, 0, 0.7]))[None], 0.0)]
+    for _ in range(6):
+        cases.append((rng.normal(size=(3, 3)), rng.normal(scale=0.6, size=(12, 3, 3)), rng.uniform(0.01, 0.1, 12)))
+    for k, (sur, ch, e) in enumerate(cases):
+        out[f"ce{k}_surrogate"] = np.asarray(sur, np.float64)
+        out[f"ce{k}_children"] = np.asarray(ch, np.float64).reshape(-1, 9)
+        out[f"ce{k}_eps"] = np.asarray(e, np.float64)
+        ce.append(conservative_epsilon(sur, ch, e))
+    out["ce_values"] = np.array(ce)
+
+
 def run() -> dict:
     from tricontact.geometry import RigidMotion
     from tricontact.kernels import KernelParams
@@ -134,6 +189,7 @@ def run() -> dict:
     spec = SceneSpec(kind="ParticleOnPlane", triangle_count=80, drop_height=0.0)
     _scene_out("plane", system_from_scene(build_scene(spec), KernelParams()), out)
     _find_contacts_cases(out)
+    _surrogate_cases(out)
     out["scenes"] = np.array(sorted({k.split("_")[0] + "_" + k.split("_")[1] if not k.startswith("plane") else "plane"
                                      for k in out if k.endswith("_checks")}))
     return out
