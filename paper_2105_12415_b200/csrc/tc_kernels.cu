@@ -28,7 +28,14 @@
 
 namespace tc {
 
-constexpr int BLOCK = 256;
+#ifndef TC_BLOCK
+#define TC_BLOCK 256
+#endif
+constexpr int BLOCK = TC_BLOCK;
+// L2 bulk prefetch of the next tile's inputs at the start of each tile
+#ifndef TC_PREFETCH
+#define TC_PREFETCH 0
+#endif
 // resident CTAs per SM the register allocator targets (launch bounds)
 #ifndef TC_ITER_MINB
 #define TC_ITER_MINB 2
@@ -309,6 +316,32 @@ __device__ __forceinline__ void load_pair(const Args<T>& a, int64_t j, R* A, R* 
     eps = R(a.eps ? a.eps[j] : a.eps_scalar);
 }
 
+// One elected thread asks the TMA unit to pull the CTA's next tile of inputs
+// into L2 (cp.async.bulk.prefetch.L2: no registers, no shared memory), so the
+// next tile's loads hit L2 instead of HBM.
+template <bool SOA, typename T>
+__device__ __forceinline__ void prefetch_tile(const Args<T>& a, int64_t tile) {
+    if (!TC_PREFETCH || threadIdx.x != 0) return;
+    const int64_t start = tile * BLOCK;
+    if (start >= a.n) return;
+    const int64_t cnt = (a.n - start) < BLOCK ? (a.n - start) : BLOCK;
+    auto pf = [](const void* p, int64_t bytes) {
+        bytes &= ~int64_t(15);
+        if (bytes > 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((unsigned)bytes) : "memory");
+    };
+    if (SOA) {
+#pragma unroll 1
+        for (int k = 0; k < 9; ++k) {
+            pf(a.tri_a + k * a.n + start, cnt * (int64_t)sizeof(T));
+            pf(a.tri_b + k * a.n + start, cnt * (int64_t)sizeof(T));
+        }
+    } else {
+        pf(a.tri_a + 9 * start, 9 * cnt * (int64_t)sizeof(T));
+        pf(a.tri_b + 9 * start, 9 * cnt * (int64_t)sizeof(T));
+    }
+}
+
 // Where the comparison phases read a queued pair from and write its result
 // to.  FlatSource: pair j of the flat (n,3,3)/SoA batch, staged into the
 // thread's shared-memory slot; results into the BatchResult columns.
@@ -537,6 +570,7 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
     __syncthreads();
     const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        prefetch_tile<SOA>(a, tile + gridDim.x);
         const int64_t i = tile * BLOCK + threadIdx.x;
         bool enq = false;
         if (i < a.n) {
