@@ -32,10 +32,16 @@ namespace tc {
 #define TC_BLOCK 256
 #endif
 constexpr int BLOCK = TC_BLOCK;
+// resident CTAs per SM for a register budget given as CTAs of 256 threads
+#define TC_MINB(n256) ((n256) * 256 / TC_BLOCK)
 // L2 bulk prefetch of the next tile's inputs at the start of each tile
 #ifndef TC_PREFETCH
-#define TC_PREFETCH 0
+#define TC_PREFETCH 1
 #endif
+// dynamic shared memory of the comparison phases, per thread (stride BLOCK):
+// [crossing list: SCR values][pair slot: SLOT values]
+constexpr int SCR = 18;
+constexpr int SLOT = 18;
 // resident CTAs per SM the register allocator targets (launch bounds)
 #ifndef TC_ITER_MINB
 #define TC_ITER_MINB 2
@@ -105,6 +111,26 @@ __device__ __forceinline__ T* thread_slot(int offset) {
     extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
     return reinterpret_cast<T*>(tc_dyn_smem) + offset + threadIdx.x;
 }
+
+// Asynchronous copy of one pair (18 values) from global memory into the
+// calling thread's slot (cp.async, LDGSTS: no registers, the copy lands while
+// the thread computes); pairs j >= n copy nothing.  One commit group per call.
+#ifndef TC_SMEM_PREFETCH
+#define TC_SMEM_PREFETCH 1
+#endif
+// (The hybrid kernel keeps one pair slot: a third slot next to the crossing
+// scratch and the comparison slot does not fit two 256-thread CTAs per SM;
+// 96-thread CTAs with three slots, and a two-pass variant that runs the
+// iterative over all tiles before the fallback, both measured slower.)
+template <typename T>
+__device__ __forceinline__ void cp_async_val(T* dst, const T* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    if constexpr (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Keep the register-resident pair in the thread's slot so the iterative
 // epilogue re-reads it from shared memory instead of global memory.
@@ -281,8 +307,8 @@ __device__ __forceinline__ Scratch<R> thread_scratch() {
 // The calling thread's planar shared-memory slot for the pair under
 // comparison (18 coordinates, stride BLOCK), after the crossing scratch.
 template <bool SOA, class R, typename T>
-__device__ __forceinline__ void stage_pair(const Args<T>& a, int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) {
-    T* slot = thread_slot<T>(18 * BLOCK);
+__device__ __forceinline__ void stage_pair(const Args<T>& a, int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps,
+                                           T* slot) {
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
         slot[k * BLOCK] = __ldg(SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
@@ -295,7 +321,7 @@ __device__ __forceinline__ void stage_pair(const Args<T>& a, int64_t j, SmemTri<
     eps = R(a.eps ? a.eps[j] : a.eps_scalar);
 }
 template <typename T>
-constexpr size_t scratch_bytes() { return sizeof(T) * 36 * BLOCK; }
+constexpr size_t scratch_bytes() { return sizeof(T) * (SCR + SLOT) * BLOCK; }
 constexpr int64_t IDS_ONLY = int64_t(1) << 62;
 
 // Warp-aggregated append (all 32 lanes of the warp must call it).
@@ -307,6 +333,18 @@ __device__ __forceinline__ void push(int64_t* q, int* n, bool pred, int64_t v) {
     if (lane == 0) base = atomicAdd(n, __popc(m));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (pred) q[base + __popc(m & ((1u << lane) - 1u))] = v;
+}
+
+template <bool SOA, typename T>
+__device__ __forceinline__ void async_pair(const Args<T>& a, int64_t j, T* slot) {
+    if (j < a.n) {
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+            cp_async_val(slot + k * BLOCK, SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
+            cp_async_val(slot + (9 + k) * BLOCK, SOA ? a.tri_b + k * a.n + j : a.tri_b + 9 * j + k);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 template <bool SOA, class R, typename T>
@@ -348,9 +386,10 @@ __device__ __forceinline__ void prefetch_tile(const Args<T>& a, int64_t tile) {
 template <bool SOA, class R, typename T>
 struct FlatSource {
     const Args<T>& a;
+    T* slot;  // the calling thread's pair slot
     __device__ __forceinline__ bool want_ids() const { return a.ids != nullptr; }
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
-        stage_pair<SOA>(a, j, A, B, eps);
+        stage_pair<SOA>(a, j, A, B, eps, slot);
     }
     __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const { store_rec<SOA>(a, j, r); }
     __device__ __forceinline__ void store_ids01(int64_t j, uint32_t ids) const {
@@ -419,7 +458,7 @@ __device__ __forceinline__ void drain(const Src& src, Queues& Q, Tally& tl, bool
 }
 
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK, 2) comparison_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BLOCK, TC_MINB(2)) comparison_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     __shared__ Queues Q;
     Tally tl;
@@ -433,7 +472,7 @@ __global__ void __launch_bounds__(BLOCK, 2) comparison_kernel(Args<T> a) {
         if (i < a.n) {
             SmemTri<R> A, B;
             R eps;
-            stage_pair<SOA>(a, i, A, B, eps);
+            stage_pair<SOA>(a, i, A, B, eps, thread_slot<T>(SCR * BLOCK));
             Rec<R> r;
             tl.comparison++;
             if (comparison_phase1(A, B, eps, thread_scratch<R>(), r)) {
@@ -448,23 +487,43 @@ __global__ void __launch_bounds__(BLOCK, 2) comparison_kernel(Args<T> a) {
         }
         push(Q.q2, &Q.n2, need2, e2);
         __syncthreads();
-        drain<R>(FlatSource<SOA, R, T>{a}, Q, tl, false, 0u);
+        drain<R>(FlatSource<SOA, R, T>{a, thread_slot<T>(SCR * BLOCK)}, Q, tl, false, 0u);
     }
-    drain<R>(FlatSource<SOA, R, T>{a}, Q, tl, true, 0u);
+    drain<R>(FlatSource<SOA, R, T>{a, thread_slot<T>(SCR * BLOCK)}, Q, tl, true, 0u);
     // comparison_batch alone counts as comparison work but not as a fallback
     tl.flush<false>(a.stats);
 }
 
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK, TC_ITER_MINB) iterative_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BLOCK, TC_MINB(TC_ITER_MINB)) iterative_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     const KP<R> kp = make_kp<R>(a);
     Tally tl;
-    for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BLOCK) {
-        R A[9], B[9], eps;
-        load_pair<SOA>(a, i, A, B, eps);
-        T* slot = thread_slot<T>(0);
-        stash_pair(slot, A, B);
+    // double-buffered pair slots filled by cp.async one tile ahead (see hybrid_kernel)
+    T* const slot0 = thread_slot<T>(0);
+    int cur = 0;
+    const int64_t stride = (int64_t)gridDim.x * BLOCK;
+    const int64_t first = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+    if (TC_SMEM_PREFETCH) async_pair<SOA>(a, first, slot0);
+    for (int64_t i = first; i - threadIdx.x < a.n; i += stride) {
+        T* slot = slot0 + cur * (SLOT * BLOCK);
+        cur ^= 1;
+        R A[9], B[9];
+        if (TC_SMEM_PREFETCH) {
+            cp_async_wait_all();
+            async_pair<SOA>(a, i + stride, slot0 + cur * (SLOT * BLOCK));
+            if (i >= a.n) continue;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                A[k] = R(slot[k * BLOCK]);
+                B[k] = R(slot[(9 + k) * BLOCK]);
+            }
+        } else {
+            if (i >= a.n) continue;
+            R eps_unused;
+            load_pair<SOA>(a, i, A, B, eps_unused);
+            stash_pair(slot, A, B);
+        }
         Rec<R> r;
         run_iterative(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
         store_rec<SOA>(a, i, r);
@@ -561,7 +620,7 @@ __global__ void __launch_bounds__(X2_THREADS, 1) iterative_kernel_x2(Args<T> a) 
 // shared-memory slots, saves the re-read of queued pairs but idles half the
 // warps: measured 8% slower on cfg1.)
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) hybrid_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     __shared__ Queues Q;
     const KP<R> kp = make_kp<R>(a);
@@ -569,6 +628,7 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
     if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
     __syncthreads();
     const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
+    T* const slot = thread_slot<T>(SCR * BLOCK);  // the comparison phases' pair slot, free here
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         prefetch_tile<SOA>(a, tile + gridDim.x);
         const int64_t i = tile * BLOCK + threadIdx.x;
@@ -576,7 +636,6 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
         if (i < a.n) {
             R A[9], B[9], eps;
             load_pair<SOA>(a, i, A, B, eps);
-            T* slot = thread_slot<T>(18 * BLOCK);  // the comparison phases' pair slot, free here
             stash_pair(slot, A, B);
             Rec<R> r;
             run_iterative(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
@@ -598,11 +657,12 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) hybrid_kernel(Args<T> a
         }
         push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
-        drain<R>(FlatSource<SOA, R, T>{a}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+        drain<R>(FlatSource<SOA, R, T>{a, slot}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
-    drain<R>(FlatSource<SOA, R, T>{a}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    drain<R>(FlatSource<SOA, R, T>{a, slot}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     tl.flush<true>(a.stats);
 }
+
 
 // ---- all-pairs particle-block kernel (BASELINE.json config 2) -----------------
 // One CTA per particle-pair block at a time (grid-stride over blocks): both
@@ -701,11 +761,11 @@ struct BlockSource {
 };
 
 template <typename T, bool STRICT>
-__global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) blocks_hybrid_kernel(BlockArgs<T> a) {
+__global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) blocks_hybrid_kernel(BlockArgs<T> a) {
     using R = typename Pol<T, STRICT>::R;
     __shared__ Queues Q;
     extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
-    T* mA = reinterpret_cast<T*>(tc_dyn_smem) + 18 * BLOCK;  // after the crossing scratch
+    T* mA = reinterpret_cast<T*>(tc_dyn_smem) + SCR * BLOCK;  // after the crossing scratch
     const int tris = a.tris;
     T* mB = mA + 9 * tris;
     const KP<R> kp = make_kp<R>(a);
@@ -851,7 +911,7 @@ struct FrontierSource {
     const FrontierArgs<T>& a;
     __device__ __forceinline__ bool want_ids() const { return false; }
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
-        T* slot = thread_slot<T>(18 * BLOCK);
+        T* slot = thread_slot<T>(SCR * BLOCK);
         const int64_t ia = a.fa[j], ib = a.fb[j];
         R X[9], Y[9];
         load_node(a, ia, X);
@@ -887,7 +947,7 @@ struct FrontierSource {
 };
 
 template <typename T, bool STRICT>
-__global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) frontier_hybrid_kernel(FrontierArgs<T> a) {
+__global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) frontier_hybrid_kernel(FrontierArgs<T> a) {
     using R = typename Pol<T, STRICT>::R;
     __shared__ Queues Q;
     __shared__ unsigned long long hist[32];
@@ -906,7 +966,7 @@ __global__ void __launch_bounds__(BLOCK, TC_HYBRID_MINB) frontier_hybrid_kernel(
             R A[9], B[9];
             load_node(a, ia, A);
             load_node(a, ib, B);
-            T* slot = thread_slot<T>(18 * BLOCK);
+            T* slot = thread_slot<T>(SCR * BLOCK);
             stash_pair(slot, A, B);
             const bool both_fine = a.is_fine[ia] && a.is_fine[ib];
             const int h = max(a.height[ia], a.height[ib]);
@@ -1086,6 +1146,21 @@ static int64_t grid_for(K kernel, int64_t n, size_t smem = 0) {
 
 enum Variant { V_COMPARISON = 0, V_ITERATIVE = 1, V_HYBRID = 2 };
 
+// Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+// pool; raising its release threshold once keeps freed blocks cached between
+// calls, so per-call workspaces cost no cudaMalloc/cudaFree synchronisation.
+static void pool_init() {
+    static std::once_flag pool_once;
+    std::call_once(pool_once, [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+}
+
 template <typename T, bool STRICT, bool SOA>
 static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
     const size_t smem = scratch_bytes<T>();  // crossing-point scratch of the comparison phases
@@ -1102,7 +1177,7 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
             k<<<(unsigned)g, X2_THREADS, 0, s>>>(a);
         } else {
             auto k = iterative_kernel<T, STRICT, SOA>;
-            const size_t ism = sizeof(T) * 18 * BLOCK;  // the pair slot of the epilogue re-reads
+            const size_t ism = sizeof(T) * 2 * SLOT * BLOCK;  // double-buffered pair slots
             k<<<(unsigned)grid_for(k, a.n, ism), BLOCK, ism, s>>>(a);
         }
     } else {
@@ -1157,7 +1232,7 @@ static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const int
     }
     if (nb == 0) return TC_OK;
     if (!meshes || !blocks) return TC_EINVAL;
-    const size_t smem = sizeof(T) * (18 * BLOCK + 18 * (size_t)tris);
+    const size_t smem = sizeof(T) * (SCR * BLOCK + 18 * (size_t)tris);
     if (smem > 200 * 1024) {
         snprintf(g_err, sizeof(g_err), "tris_per_mesh %d too large for shared-memory staging", tris);
         return TC_EINVAL;
@@ -1201,19 +1276,9 @@ static int run_multiscale(const T* tris, const int32_t* owner, const T* motions,
     if (n_pairs == 0) return TC_OK;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e;
-    // device scratch: frontier (two generations), kind, counts/offsets, tallies
-    // stream-ordered allocations from the device's default pool, kept cached
-    // between calls (release threshold raised once) so a call costs no
-    // cudaMalloc/cudaFree synchronisation
-    static std::once_flag pool_once;
-    std::call_once(pool_once, [] {
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-    });
+    // device scratch (frontier, kind, counts/offsets, tallies) from the
+    // stream-ordered pool: a call costs no cudaMalloc/cudaFree synchronisation
+    pool_init();
     struct Buf {
         void* p = nullptr;
         cudaStream_t s = nullptr;
