@@ -39,8 +39,9 @@ constexpr int BLOCK = TC_BLOCK;
 #define TC_PREFETCH 1
 #endif
 // dynamic shared memory of the comparison phases, per thread (stride BLOCK):
-// [crossing list: SCR values][pair slot: SLOT values]
-constexpr int SCR = 18;
+// [crossing points: SCR values (at most 4 points, see comparison_phase1)]
+// [pair slot: SLOT values]
+constexpr int SCR = 12;
 constexpr int SLOT = 18;
 // resident CTAs per SM the register allocator targets (launch bounds)
 #ifndef TC_ITER_MINB
@@ -118,10 +119,11 @@ __device__ __forceinline__ T* thread_slot(int offset) {
 #ifndef TC_SMEM_PREFETCH
 #define TC_SMEM_PREFETCH 1
 #endif
-// (The hybrid kernel keeps one pair slot: a third slot next to the crossing
-// scratch and the comparison slot does not fit two 256-thread CTAs per SM;
-// 96-thread CTAs with three slots, and a two-pass variant that runs the
-// iterative over all tiles before the fallback, both measured slower.)
+// (Tried and measured slower for the hybrid kernel: a second pair slot filled
+// by cp.async (the shared-memory growth shrinks L1, which holds the queued
+// pairs' re-reads and the spills), 96-thread CTAs with a double-buffered
+// slot, and a two-pass variant that runs the iterative over all of a CTA's
+// tiles before its fallback.)
 template <typename T>
 __device__ __forceinline__ void cp_async_val(T* dst, const T* src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -294,7 +296,7 @@ struct Queues {
     int n1, n2;
 };
 
-// Shared-memory crossing-point scratch of the calling thread (6 x 3 values).
+// Shared-memory crossing-point scratch of the calling thread (4 x 3 values).
 template <class R>
 __device__ __forceinline__ Scratch<R> thread_scratch() {
     using T = typename Store<R>::type;

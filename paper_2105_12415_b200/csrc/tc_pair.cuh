@@ -310,7 +310,9 @@ __device__ __forceinline__ bool segment_crosses(const R* p, const R* q, const Tr
 //
 // Phase 1: the six edge-plane tests (RK/kernels.py:364-375).  Valid crossing
 // points go to a small per-thread list in shared memory (usually 0 or 2
-// entries); the farthest pair is kept with the reference's first-argmax
+// entries, at most 4: a proper crossing needs the edge's two vertex-plane
+// distances of strictly opposite sign, and around a triangle's 3-cycle of
+// vertices at most 2 edges change sign -- per triangle); the farthest pair is kept with the reference's first-argmax
 // order over the row-major 6x6 grid.  An intersecting pair is complete
 // after this phase: distance 0, both points at the midpoint, barycentric
 // coordinates of the midpoint on A and B (RK/kernels.py:377-398).
