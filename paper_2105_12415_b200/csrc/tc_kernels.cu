@@ -535,83 +535,9 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(TC_ITER_MINB)) iterative_kernel
     tl.flush<false>(a.stats);
 }
 
-// Experiment (TC_ITER_X2): the fast iterative kernel with two pairs per
-// thread interleaved (twice the independent FP64 chains per warp), 384
-// threads per CTA, pairs re-read from global memory in the epilogue.
-#ifndef TC_ITER_X2
-#define TC_ITER_X2 0
-#endif
-constexpr int X2_THREADS = 384;
-template <typename T, bool SOA>
-__global__ void __launch_bounds__(X2_THREADS, 1) iterative_kernel_x2(Args<T> a) {
-    using R = T;
-    const KP<R> kp = make_kp<R>(a);
-    Tally tl;
-    const int64_t per_tile = 2 * X2_THREADS;
-    for (int64_t base = (int64_t)blockIdx.x * per_tile; base < a.n; base += (int64_t)gridDim.x * per_tile) {
-        int64_t idx[2] = {base + threadIdx.x, base + X2_THREADS + threadIdx.x};
-        GramSolver<true, R> gs[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int64_t i = idx[q] < a.n ? idx[q] : a.n - 1;
-            R A[9], B[9];
-            load_tri<SOA>(a.tri_a, i, a.n, A);
-            load_tri<SOA>(a.tri_b, i, a.n, B);
-            gs[q].init(A, B, kp);
-        }
-#pragma unroll 1
-        for (int it = 0; it < kp.n_iterative - 1; ++it) {
-            gs[0].sweep();
-            gs[1].sweep();
-        }
-        typename GramSolver<true, R>::Pre pre[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int64_t i = idx[q] < a.n ? idx[q] : a.n - 1;
-            auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4, R* sq, R* eps_out) {
-                R At[9], Bt[9];
-                load_tri<SOA>(a.tri_a, i, a.n, At);
-                load_tri<SOA>(a.tri_b, i, a.n, Bt);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    A0[k] = At[k]; B0[k] = Bt[k];
-                    E0[k] = At[3 + k] - At[k]; E1[k] = At[6 + k] - At[k];
-                    E3[k] = Bt[k] - Bt[3 + k]; E4[k] = Bt[k] - Bt[6 + k];
-                }
-                if (sq) {
-                    *sq = maxv(max_sq_edge(At), max_sq_edge(Bt));
-                    *eps_out = R(a.eps ? a.eps[i] : a.eps_scalar);
-                }
-            };
-            gs[q].prelast(reload, kp, pre[q]);
-        }
-        gs[0].sweep();
-        gs[1].sweep();
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int64_t i = idx[q] < a.n ? idx[q] : a.n - 1;
-            auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4, R*, R*) {
-                R At[9], Bt[9];
-                load_tri<SOA>(a.tri_a, i, a.n, At);
-                load_tri<SOA>(a.tri_b, i, a.n, Bt);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    A0[k] = At[k]; B0[k] = Bt[k];
-                    E0[k] = At[3 + k] - At[k]; E1[k] = At[6 + k] - At[k];
-                    E3[k] = Bt[k] - Bt[3 + k]; E4[k] = Bt[k] - Bt[6 + k];
-                }
-            };
-            Rec<R> r;
-            gs[q].finish(reload, kp, pre[q], r);
-            if (idx[q] < a.n) {
-                store_rec<SOA>(a, idx[q], r);
-                tl.iterative++;
-                tl.result(r);
-            }
-        }
-    }
-    (void)tl;  // stats are not tallied by this experiment
-}
+// (Tried: two pairs per thread interleaved, 384 threads per CTA -- twice the
+// independent FP64 chains per warp but one CTA per SM at the register cap;
+// measured slower than two 256-thread CTAs.)
 
 // RK/kernels.py:568-605.  Per tile of BLOCK pairs: the iterative kernel on
 // every lane; open (NOT_TERMINATED, fallback allowed, non-degenerate) pairs
@@ -1170,18 +1096,9 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         auto k = comparison_kernel<T, STRICT, SOA>;
         k<<<(unsigned)grid_for(k, a.n, smem), BLOCK, smem, s>>>(a);
     } else if (variant == V_ITERATIVE) {
-        if (TC_ITER_X2 && !STRICT) {
-            auto k = iterative_kernel_x2<T, SOA>;
-            int per_sm = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, X2_THREADS, 0);
-            const int64_t tiles = (a.n + 2 * X2_THREADS - 1) / (2 * X2_THREADS);
-            const int64_t g = std::min<int64_t>(tiles, (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1));
-            k<<<(unsigned)g, X2_THREADS, 0, s>>>(a);
-        } else {
-            auto k = iterative_kernel<T, STRICT, SOA>;
-            const size_t ism = sizeof(T) * 2 * SLOT * BLOCK;  // double-buffered pair slots
-            k<<<(unsigned)grid_for(k, a.n, ism), BLOCK, ism, s>>>(a);
-        }
+        auto k = iterative_kernel<T, STRICT, SOA>;
+        const size_t ism = sizeof(T) * 2 * SLOT * BLOCK;  // double-buffered pair slots
+        k<<<(unsigned)grid_for(k, a.n, ism), BLOCK, ism, s>>>(a);
     } else {
         auto k = hybrid_kernel<T, STRICT, SOA>;
         k<<<(unsigned)grid_for(k, a.n, smem), BLOCK, smem, s>>>(a);
