@@ -251,54 +251,54 @@ __device__ __forceinline__ void edge_bary(int k, R s, R* o) {
 }
 
 // Per-target-triangle constants of the edge-plane test (RK/kernels.py:269-298).
+// The edge vectors u, v and the origin a are kept too: every edge test and
+// vertex distance uses the same values the reference computes once per
+// triangle, so hoisting them is exact in both arithmetic policies.
 template <class R>
 struct PlaneFrame {
-    R nrm[3], uu, uv, vv, det_safe, rdet;
+    R a[3], u[3], v[3], nrm[3], uu, uv, vv, det_safe, rdet;
 };
 
 template <class R, class Tri>
 __device__ __forceinline__ void plane_frame(const Tri& tri, PlaneFrame<R>& f) {
     const R tiny = R(Tiny<R>::v);
-    R u[3], v[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-        const R a = tri[i];
-        u[i] = tri[3 + i] - a;
-        v[i] = tri[6 + i] - a;
+        f.a[i] = tri[i];
+        f.u[i] = tri[3 + i] - f.a[i];
+        f.v[i] = tri[6 + i] - f.a[i];
     }
-    cross3(u, v, f.nrm);
-    f.uu = dot3(u, u);
-    f.uv = dot3(u, v);
-    f.vv = dot3(v, v);
+    cross3(f.u, f.v, f.nrm);
+    f.uu = dot3(f.u, f.u);
+    f.uv = dot3(f.u, f.v);
+    f.vv = dot3(f.v, f.v);
     const R det = f.uu * f.vv - f.uv * f.uv;
     f.det_safe = (absv(det) > tiny) ? det : R(1);
     f.rdet = rcpv(f.det_safe);
 }
 
-// One proper crossing test of segment [p, q] through the closed triangle.
-template <class R, class Tri>
-__device__ __forceinline__ bool segment_crosses(const R* p, const R* q, const Tri& tri, const PlaneFrame<R>& f, R* x) {
-    R t3[3], u[3], v[3], a[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) a[i] = tri[i];
-    sub3(p, a, t3);
-    const R dp = dot3(t3, f.nrm);
-    sub3(q, a, t3);
-    const R dq = dot3(t3, f.nrm);
+// Signed distance (times |n|) of a point from the frame's plane.
+template <class R>
+__device__ __forceinline__ R plane_dist(const R* p, const PlaneFrame<R>& f) {
+    R t3[3];
+    sub3(p, f.a, t3);
+    return dot3(t3, f.nrm);
+}
+
+// One proper crossing test of segment [p, q] through the closed triangle,
+// given the endpoints' plane distances dp, dq (plane_dist).
+template <class R>
+__device__ __forceinline__ bool segment_crosses(const R* p, const R* q, R dp, R dq, const PlaneFrame<R>& f, R* x) {
+    R t3[3];
     const bool crossing = (dp * dq) < R(0);
     const R denom = dp - dq;
     const R t = divv(dp, denom == R(0) ? R(1) : denom);
     sub3(q, p, t3);
 #pragma unroll
     for (int i = 0; i < 3; ++i) x[i] = p[i] + t * t3[i];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        u[i] = tri[3 + i] - a[i];
-        v[i] = tri[6 + i] - a[i];
-    }
-    sub3(x, a, t3);
-    const R wu = dot3(t3, u);
-    const R wv = dot3(t3, v);
+    sub3(x, f.a, t3);
+    const R wu = dot3(t3, f.u);
+    const R wv = dot3(t3, f.v);
     const R b1 = divr(f.vv * wu - f.uv * wv, f.det_safe, f.rdet);
     const R b2 = divr(f.uu * wv - f.uv * wu, f.det_safe, f.rdet);
     return crossing && (b1 >= R(0)) && (b2 >= R(0)) && ((b1 + b2) <= R(1));
@@ -341,12 +341,20 @@ __device__ __forceinline__ bool comparison_phase1(const Tri& A, const Tri& B, R 
     {
         PlaneFrame<R> fb;
         plane_frame(B, fb);
+        R s0, s1, s2;  // A's vertices against B's plane (each shared by two edges)
+        {
+            R v[3];
+            A.vertex(0, v); s0 = plane_dist(v, fb);
+            A.vertex(1, v); s1 = plane_dist(v, fb);
+            A.vertex(2, v); s2 = plane_dist(v, fb);
+        }
 #pragma unroll kUnrollX
         for (int k = 0; k < 3; ++k) {
             R p[3], q[3], x[3];
             A.vertex(edge_start(k), p);
             A.vertex(edge_end(k), q);
-            if (segment_crosses(p, q, B, fb, x)) {
+            const R dp = k == 0 ? s0 : (k == 1 ? s1 : s2), dq = k == 0 ? s1 : (k == 1 ? s2 : s0);
+            if (segment_crosses(p, q, dp, dq, fb, x)) {
                 cpts.put(nv, x);
                 ck |= k << (3 * nv);
                 ++nv;
@@ -354,12 +362,19 @@ __device__ __forceinline__ bool comparison_phase1(const Tri& A, const Tri& B, R 
         }
         PlaneFrame<R> fa;
         plane_frame(A, fa);
+        {
+            R v[3];
+            B.vertex(0, v); s0 = plane_dist(v, fa);  // (reuses s0-s2: B's vertices vs A's plane)
+            B.vertex(1, v); s1 = plane_dist(v, fa);
+            B.vertex(2, v); s2 = plane_dist(v, fa);
+        }
 #pragma unroll kUnrollX
         for (int k = 0; k < 3; ++k) {
             R p[3], q[3], x[3];
             B.vertex(edge_start(k), p);
             B.vertex(edge_end(k), q);
-            if (segment_crosses(p, q, A, fa, x)) {
+            const R dp = k == 0 ? s0 : (k == 1 ? s1 : s2), dq = k == 0 ? s1 : (k == 1 ? s2 : s0);
+            if (segment_crosses(p, q, dp, dq, fa, x)) {
                 cpts.put(nv, x);
                 ck |= (3 + k) << (3 * nv);
                 ++nv;
