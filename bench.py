@@ -399,9 +399,50 @@ def e2e_measure(lib, _abi, torch, A, B, n, world, dist, dev, reps=3):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     sec = float(t[0])
+    link = pcie_probe(torch, dev)
+    # the transfers are the floor: while both directions run each gets the
+    # duplex rate, then the larger direction finishes alone at its own rate
+    h, d = n * 144, n * 89
+    both = min(h, d) / (link["duplex_gbs_per_direction"] * 1e9)
+    rest = (h - d) / (link["h2d_gbs"] * 1e9) if h > d else (d - h) / (link["d2h_gbs"] * 1e9)
+    floor = both + rest
+    link["floor_ms"] = 1e3 * floor
+    link["frac_of_floor"] = floor / sec
+    link["note"] = "pinned copies on this box; floor = PCIe time of the step's H2D + D2H bytes"
     return {"value": n * world / sec, "unit": UNIT, "h2d_bytes_per_step": n * 144 * world,
             "d2h_bytes_per_step": n * 89 * world, "ms_per_step": 1e3 * sec,
-            "path": "tc_run_host_f64 (host C ABI, pinned, 1M-pair chunks on 3 streams)"}
+            "path": "tc_run_host_f64 (host C ABI, pinned, 1M-pair chunks on 3 streams)", "link": link}
+
+
+def pcie_probe(torch, dev, mb=512, reps=5):
+    """Pinned host<->device copy bandwidth on this box (GB/s), each direction
+    alone: the e2e path's transfer floor."""
+    h = torch.empty(mb << 20, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(mb << 20, dtype=torch.uint8, device=dev)
+    res = {}
+    for name, dst, src in (("h2d_gbs", d, h), ("d2h_gbs", h, d)):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        res[name] = reps * (mb << 20) / (e0.elapsed_time(e1) / 1e3) / 1e9
+    # both directions at once (two streams): the duplex rate per direction
+    h2, d2 = torch.empty_like(h).pin_memory(), torch.empty_like(d)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+    torch.cuda.synchronize()
+    res["duplex_gbs_per_direction"] = reps * (mb << 20) / (time.perf_counter() - t0) / 1e9
+    return res
 
 
 def configs_table(D, torch, dev):

@@ -1366,7 +1366,11 @@ static int run_host(int variant, const T* tri_a, const T* tri_b, int64_t n, cons
         if ((e = cudaMalloc(&h.dstats, sizeof(tc_stats))) != cudaSuccess) return set_err("cudaMalloc", e);
         h.init = true;
     }
-    const int64_t chunk = 1 << 20;
+    static const int64_t chunk = [] {
+        const char* v = getenv("TC_HOST_CHUNK");  // pairs per pipeline chunk (tuning knob)
+        const long long c = v ? atoll(v) : 0;
+        return (int64_t)(c >= 4096 ? c : (1 << 20));
+    }();
     const bool want_ids = (p->flags & TC_EMIT_IDS) && ids;
     // per-pair bytes staged: inputs, eps, allow, outputs
     const size_t per = sizeof(T) * (18 + 1 + 11) + 2 + (want_ids ? 4 : 0);
