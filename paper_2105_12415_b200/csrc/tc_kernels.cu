@@ -28,12 +28,34 @@
 
 namespace tc {
 
-#ifndef TC_BLOCK
-#define TC_BLOCK 256
+// CTA sizes.  BLOCK (256) serves the one-pair-per-thread helpers and is the
+// largest CTA; the batched kernels pick their own size (measured on cfg1):
+// the iterative and all-pairs block kernels run 256-thread CTAs, the hybrid,
+// comparison and multiscale-frontier kernels 128-thread CTAs, whose queue
+// batches and per-tile barriers span half as many warps (+3 % hybrid,
+// +5 % comparison; the iterative kernel loses 3 % at 128).  Device helpers
+// read the CTA size from blockDim.x.
+constexpr int BLOCK = 256;
+#ifndef TC_BS_ITER
+#define TC_BS_ITER 256
 #endif
-constexpr int BLOCK = TC_BLOCK;
-// resident CTAs per SM for a register budget given as CTAs of 256 threads
-#define TC_MINB(n256) ((n256) * 256 / TC_BLOCK)
+#ifndef TC_BS_HYB
+#define TC_BS_HYB 128
+#endif
+#ifndef TC_BS_CMP
+#define TC_BS_CMP 128
+#endif
+#ifndef TC_BS_BLK
+#define TC_BS_BLK 256
+#endif
+#ifndef TC_BS_FRONT
+#define TC_BS_FRONT 128
+#endif
+constexpr int BS_ITER = TC_BS_ITER, BS_HYB = TC_BS_HYB, BS_CMP = TC_BS_CMP, BS_BLK = TC_BS_BLK,
+              BS_FRONT = TC_BS_FRONT;
+// resident CTAs per SM of a bs-thread kernel for a register budget given as
+// CTAs of 256 threads (launch bounds)
+#define TC_MINB(bs, n256) ((n256) * 256 / (bs))
 // L2 bulk prefetch of the next tile's inputs at the start of each tile
 #ifndef TC_PREFETCH
 #define TC_PREFETCH 1
@@ -136,12 +158,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // Keep the register-resident pair in the thread's slot so the iterative
 // epilogue re-reads it from shared memory instead of global memory.
-template <class R, typename T>
+template <int BS, class R, typename T>
 __device__ __forceinline__ void stash_pair(T* slot, const R* A, const R* B) {
+    constexpr int bs = BS;
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
-        slot[k * BLOCK] = val(A[k]);
-        slot[(9 + k) * BLOCK] = val(B[k]);
+        slot[k * bs] = val(A[k]);
+        slot[(9 + k) * bs] = val(B[k]);
     }
 }
 
@@ -183,10 +206,11 @@ __device__ __forceinline__ void run_iterative(const TA& SA, const TB& SB, const 
         else iterative_pair_gram<false>(A, B, kp, r, reload);
     }
 }
-template <class R, typename T, class EpsFn>
+template <int BS, class R, typename T, class EpsFn>
 __device__ __forceinline__ void run_iterative(const T* slot, const R* A, const R* B, EpsFn eps_fn, const KP<R>& kp,
                                               Rec<R>& r) {
-    run_iterative(SmemTri<R>{slot, BLOCK}, SmemTri<R>{slot + 9 * BLOCK, BLOCK}, A, B, eps_fn, kp, r);
+    constexpr int bs = BS;
+    run_iterative(SmemTri<R>{slot, bs}, SmemTri<R>{slot + 9 * bs, bs}, A, B, eps_fn, kp, r);
 }
 
 template <bool SOA, class R, typename T>
@@ -259,7 +283,7 @@ struct Tally {
         if (threadIdx.x == 0) {
             unsigned long long v[5] = {0, 0, 0, 0, 0};
             double m = __builtin_huge_val();
-            for (int w = 0; w < BLOCK / 32; ++w) {
+            for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
                 for (int k = 0; k < 5; ++k) v[k] += red[k][w];
                 m = (redm[w] < m) ? redm[w] : m;
             }
@@ -290,40 +314,42 @@ struct Pol<T, true> { using R = Strict<T>; };
 // Block-shared work queues of pair indices for the compacted comparison
 // phases: q1 holds pairs awaiting phase 1 (crossings), q2 pairs awaiting
 // phase 2 (features).  Bit 62 of a q2 entry marks "ids only".
+template <int QB>  // the CTA size: one batch
 struct Queues {
-    int64_t q1[2 * BLOCK];
-    int64_t q2[2 * BLOCK];
+    int64_t q1[2 * QB];
+    int64_t q2[2 * QB];
     int n1, n2;
 };
 
 // Shared-memory crossing-point scratch of the calling thread (4 x 3 values).
-template <class R>
+template <class R, int BS>
 __device__ __forceinline__ Scratch<R> thread_scratch() {
     using T = typename Store<R>::type;
     extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
     Scratch<R> s;
     s.p = reinterpret_cast<T*>(tc_dyn_smem) + threadIdx.x;
-    s.stride = BLOCK;
+    s.stride = BS;
     return s;
 }
 // The calling thread's planar shared-memory slot for the pair under
 // comparison (18 coordinates, stride BLOCK), after the crossing scratch.
-template <bool SOA, class R, typename T>
+template <bool SOA, int BS, class R, typename T>
 __device__ __forceinline__ void stage_pair(const Args<T>& a, int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps,
                                            T* slot) {
+    constexpr int bs = BS;
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
-        slot[k * BLOCK] = __ldg(SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
-        slot[(9 + k) * BLOCK] = __ldg(SOA ? a.tri_b + k * a.n + j : a.tri_b + 9 * j + k);
+        slot[k * bs] = __ldg(SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
+        slot[(9 + k) * bs] = __ldg(SOA ? a.tri_b + k * a.n + j : a.tri_b + 9 * j + k);
     }
     A.p = slot;
-    A.stride = BLOCK;
-    B.p = slot + 9 * BLOCK;
-    B.stride = BLOCK;
+    A.stride = bs;
+    B.p = slot + 9 * bs;
+    B.stride = bs;
     eps = R(a.eps ? a.eps[j] : a.eps_scalar);
 }
 template <typename T>
-constexpr size_t scratch_bytes() { return sizeof(T) * (SCR + SLOT) * BLOCK; }
+constexpr size_t scratch_bytes(int bs) { return sizeof(T) * (SCR + SLOT) * bs; }
 constexpr int64_t IDS_ONLY = int64_t(1) << 62;
 
 // Warp-aggregated append (all 32 lanes of the warp must call it).
@@ -337,13 +363,14 @@ __device__ __forceinline__ void push(int64_t* q, int* n, bool pred, int64_t v) {
     if (pred) q[base + __popc(m & ((1u << lane) - 1u))] = v;
 }
 
-template <bool SOA, typename T>
+template <bool SOA, int BS, typename T>
 __device__ __forceinline__ void async_pair(const Args<T>& a, int64_t j, T* slot) {
     if (j < a.n) {
+        constexpr int bs = BS;
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-            cp_async_val(slot + k * BLOCK, SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
-            cp_async_val(slot + (9 + k) * BLOCK, SOA ? a.tri_b + k * a.n + j : a.tri_b + 9 * j + k);
+            cp_async_val(slot + k * bs, SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
+            cp_async_val(slot + (9 + k) * bs, SOA ? a.tri_b + k * a.n + j : a.tri_b + 9 * j + k);
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -359,12 +386,13 @@ __device__ __forceinline__ void load_pair(const Args<T>& a, int64_t j, R* A, R* 
 // One elected thread asks the TMA unit to pull the CTA's next tile of inputs
 // into L2 (cp.async.bulk.prefetch.L2: no registers, no shared memory), so the
 // next tile's loads hit L2 instead of HBM.
-template <bool SOA, typename T>
+template <bool SOA, int BS, typename T>
 __device__ __forceinline__ void prefetch_tile(const Args<T>& a, int64_t tile) {
     if (!TC_PREFETCH || threadIdx.x != 0) return;
-    const int64_t start = tile * BLOCK;
+    constexpr int bs = BS;
+    const int64_t start = tile * bs;
     if (start >= a.n) return;
-    const int64_t cnt = (a.n - start) < BLOCK ? (a.n - start) : BLOCK;
+    const int64_t cnt = (a.n - start) < bs ? (a.n - start) : bs;
     auto pf = [](const void* p, int64_t bytes) {
         bytes &= ~int64_t(15);
         if (bytes > 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0)
@@ -385,13 +413,13 @@ __device__ __forceinline__ void prefetch_tile(const Args<T>& a, int64_t tile) {
 // Where the comparison phases read a queued pair from and write its result
 // to.  FlatSource: pair j of the flat (n,3,3)/SoA batch, staged into the
 // thread's shared-memory slot; results into the BatchResult columns.
-template <bool SOA, class R, typename T>
+template <bool SOA, class R, typename T, int BS>
 struct FlatSource {
     const Args<T>& a;
     T* slot;  // the calling thread's pair slot
     __device__ __forceinline__ bool want_ids() const { return a.ids != nullptr; }
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
-        stage_pair<SOA>(a, j, A, B, eps, slot);
+        stage_pair<SOA, BS>(a, j, A, B, eps, slot);
     }
     __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const { store_rec<SOA>(a, j, r); }
     __device__ __forceinline__ void store_ids01(int64_t j, uint32_t ids) const {
@@ -400,21 +428,22 @@ struct FlatSource {
     }
 };
 
-// Run whole batches (BLOCK pairs, or the remainder when `final_`) from the
-// queues until neither holds a full batch.  Block-uniform; every batch runs
-// on full warps.  `fallback_flag`: hybrid results carry FLAG_FALLBACK.
-template <class R, class Src>
-__device__ __forceinline__ void drain(const Src& src, Queues& Q, Tally& tl, bool final_, uint32_t fallback_flag) {
+// Run whole batches (QB pairs -- the CTA size --, or the remainder when
+// `final_`) from the queues until neither holds a full batch.  Block-uniform;
+// every batch runs on full warps.  `fallback_flag`: hybrid results carry
+// FLAG_FALLBACK.
+template <class R, class Src, int QB>
+__device__ __forceinline__ void drain(const Src& src, Queues<QB>& Q, Tally& tl, bool final_, uint32_t fallback_flag) {
     const bool want_ids = src.want_ids();
     while (true) {
         const int c1 = Q.n1, c2 = Q.n2;
         __syncthreads();  // everyone has read the counts before they change
         int which = 0;
-        if (c1 >= BLOCK || (final_ && c1 > 0)) which = 1;
-        else if (c2 >= BLOCK || (final_ && c2 > 0)) which = 2;
+        if (c1 >= QB || (final_ && c1 > 0)) which = 1;
+        else if (c2 >= QB || (final_ && c2 > 0)) which = 2;
         if (!which) break;
         const int c = which == 1 ? c1 : c2;
-        const int m = c < BLOCK ? c : BLOCK;
+        const int m = c < QB ? c : QB;
         int64_t e = -1;
         if ((int)threadIdx.x < m) e = (which == 1 ? Q.q1 : Q.q2)[c - m + threadIdx.x];
         __syncthreads();
@@ -432,7 +461,7 @@ __device__ __forceinline__ void drain(const Src& src, Queues& Q, Tally& tl, bool
             Rec<R> r;
             if (which == 1) {
                 tl.comparison++;
-                if (comparison_phase1(A, B, eps, thread_scratch<R>(), r)) {
+                if (comparison_phase1(A, B, eps, thread_scratch<R, QB>(), r)) {
                     r.ids |= fallback_flag << 24;
                     src.store(j, r);
                     tl.result(r);
@@ -460,24 +489,24 @@ __device__ __forceinline__ void drain(const Src& src, Queues& Q, Tally& tl, bool
 }
 
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK, TC_MINB(2)) comparison_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BS_CMP, TC_MINB(BS_CMP, 2)) comparison_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
-    __shared__ Queues Q;
+    __shared__ Queues<BS_CMP> Q;
     Tally tl;
     if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
     __syncthreads();
-    const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
+    const int64_t ntiles = (a.n + BS_CMP - 1) / BS_CMP;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t i = tile * BLOCK + threadIdx.x;
+        const int64_t i = tile * BS_CMP + threadIdx.x;
         bool need2 = false;
         int64_t e2 = 0;
         if (i < a.n) {
             SmemTri<R> A, B;
             R eps;
-            stage_pair<SOA>(a, i, A, B, eps, thread_slot<T>(SCR * BLOCK));
+            stage_pair<SOA, BS_CMP>(a, i, A, B, eps, thread_slot<T>(SCR * BS_CMP));
             Rec<R> r;
             tl.comparison++;
-            if (comparison_phase1(A, B, eps, thread_scratch<R>(), r)) {
+            if (comparison_phase1(A, B, eps, thread_scratch<R, BS_CMP>(), r)) {
                 store_rec<SOA>(a, i, r);
                 tl.result(r);
                 need2 = a.ids != nullptr;
@@ -489,45 +518,45 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(2)) comparison_kernel(Args<T> a
         }
         push(Q.q2, &Q.n2, need2, e2);
         __syncthreads();
-        drain<R>(FlatSource<SOA, R, T>{a, thread_slot<T>(SCR * BLOCK)}, Q, tl, false, 0u);
+        drain<R>(FlatSource<SOA, R, T, BS_CMP>{a, thread_slot<T>(SCR * BS_CMP)}, Q, tl, false, 0u);
     }
-    drain<R>(FlatSource<SOA, R, T>{a, thread_slot<T>(SCR * BLOCK)}, Q, tl, true, 0u);
+    drain<R>(FlatSource<SOA, R, T, BS_CMP>{a, thread_slot<T>(SCR * BS_CMP)}, Q, tl, true, 0u);
     // comparison_batch alone counts as comparison work but not as a fallback
     tl.flush<false>(a.stats);
 }
 
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK, TC_MINB(TC_ITER_MINB)) iterative_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BS_ITER, TC_MINB(BS_ITER, TC_ITER_MINB)) iterative_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     const KP<R> kp = make_kp<R>(a);
     Tally tl;
     // double-buffered pair slots filled by cp.async one tile ahead (see hybrid_kernel)
     T* const slot0 = thread_slot<T>(0);
     int cur = 0;
-    const int64_t stride = (int64_t)gridDim.x * BLOCK;
-    const int64_t first = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-    if (TC_SMEM_PREFETCH) async_pair<SOA>(a, first, slot0);
+    const int64_t stride = (int64_t)gridDim.x * BS_ITER;
+    const int64_t first = (int64_t)blockIdx.x * BS_ITER + threadIdx.x;
+    if (TC_SMEM_PREFETCH) async_pair<SOA, BS_ITER>(a, first, slot0);
     for (int64_t i = first; i - threadIdx.x < a.n; i += stride) {
-        T* slot = slot0 + cur * (SLOT * BLOCK);
+        T* slot = slot0 + cur * (SLOT * BS_ITER);
         cur ^= 1;
         R A[9], B[9];
         if (TC_SMEM_PREFETCH) {
             cp_async_wait_all();
-            async_pair<SOA>(a, i + stride, slot0 + cur * (SLOT * BLOCK));
+            async_pair<SOA, BS_ITER>(a, i + stride, slot0 + cur * (SLOT * BS_ITER));
             if (i >= a.n) continue;
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
-                A[k] = R(slot[k * BLOCK]);
-                B[k] = R(slot[(9 + k) * BLOCK]);
+                A[k] = R(slot[k * BS_ITER]);
+                B[k] = R(slot[(9 + k) * BS_ITER]);
             }
         } else {
             if (i >= a.n) continue;
             R eps_unused;
             load_pair<SOA>(a, i, A, B, eps_unused);
-            stash_pair(slot, A, B);
+            stash_pair<BS_ITER>(slot, A, B);
         }
         Rec<R> r;
-        run_iterative(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
+        run_iterative<BS_ITER>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
         store_rec<SOA>(a, i, r);
         tl.iterative++;
         tl.result(r);
@@ -548,28 +577,28 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(TC_ITER_MINB)) iterative_kernel
 // shared-memory slots, saves the re-read of queued pairs but idles half the
 // warps: measured 8% slower on cfg1.)
 template <typename T, bool STRICT, bool SOA>
-__global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) hybrid_kernel(Args<T> a) {
+__global__ void __launch_bounds__(BS_HYB, TC_MINB(BS_HYB, TC_HYBRID_MINB)) hybrid_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
-    __shared__ Queues Q;
+    __shared__ Queues<BS_HYB> Q;
     const KP<R> kp = make_kp<R>(a);
     Tally tl;
     if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
     __syncthreads();
-    const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
-    T* const slot = thread_slot<T>(SCR * BLOCK);  // the comparison phases' pair slot, free here
+    const int64_t ntiles = (a.n + BS_HYB - 1) / BS_HYB;
+    T* const slot = thread_slot<T>(SCR * BS_HYB);  // the comparison phases' pair slot, free here
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        prefetch_tile<SOA>(a, tile + gridDim.x);
-        const int64_t i = tile * BLOCK + threadIdx.x;
+        prefetch_tile<SOA, BS_HYB>(a, tile + gridDim.x);
+        const int64_t i = tile * BS_HYB + threadIdx.x;
         bool enq = false;
         if (i < a.n) {
             R A[9], B[9], eps;
             load_pair<SOA>(a, i, A, B, eps);
-            stash_pair(slot, A, B);
+            stash_pair<BS_HYB>(slot, A, B);
             Rec<R> r;
-            run_iterative(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
+            run_iterative<BS_HYB>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
             tl.iterative++;
             if (r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i])) {
-                const SmemTri<R> SA{slot, BLOCK}, SB{slot + 9 * BLOCK, BLOCK};
+                const SmemTri<R> SA{slot, BS_HYB}, SB{slot + 9 * BS_HYB, BS_HYB};
                 if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {
                     r.kind = KIND_DEGENERATE;
                     r.ids |= (uint32_t)FLAG_DEGENERATE << 24;
@@ -585,9 +614,9 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) hybrid_kernel(
         }
         push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
-        drain<R>(FlatSource<SOA, R, T>{a, slot}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+        drain<R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
-    drain<R>(FlatSource<SOA, R, T>{a, slot}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    drain<R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     tl.flush<true>(a.stats);
 }
 
@@ -689,11 +718,11 @@ struct BlockSource {
 };
 
 template <typename T, bool STRICT>
-__global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) blocks_hybrid_kernel(BlockArgs<T> a) {
+__global__ void __launch_bounds__(BS_BLK, TC_MINB(BS_BLK, TC_HYBRID_MINB)) blocks_hybrid_kernel(BlockArgs<T> a) {
     using R = typename Pol<T, STRICT>::R;
-    __shared__ Queues Q;
+    __shared__ Queues<BS_BLK> Q;
     extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
-    T* mA = reinterpret_cast<T*>(tc_dyn_smem) + SCR * BLOCK;  // after the crossing scratch
+    T* mA = reinterpret_cast<T*>(tc_dyn_smem) + SCR * BS_BLK;  // after the crossing scratch
     const int tris = a.tris;
     T* mB = mA + 9 * tris;
     const KP<R> kp = make_kp<R>(a);
@@ -705,7 +734,7 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) blocks_hybrid_
         // a mesh against itself skips the diagonal (RK/contact.py:119-124)
         const bool self = ia == ib;
         const int64_t P = (int64_t)na * nbt;
-        const int64_t ntile = (P + BLOCK - 1) / BLOCK;
+        const int64_t ntile = (P + BS_BLK - 1) / BS_BLK;
         const T* gA = a.meshes + ia * tris * 9;
         const T* gB = a.meshes + ib * tris * 9;
         if (a.motions) {
@@ -714,7 +743,7 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) blocks_hybrid_
             R RA[9], tA[3], RB[9], tB[3];
             motion_matrix(a.motions + 7 * ia, RA, tA);
             motion_matrix(a.motions + 7 * ib, RB, tB);
-            for (int e = threadIdx.x; e < 3 * max(na, nbt); e += BLOCK) {
+            for (int e = threadIdx.x; e < 3 * max(na, nbt); e += BS_BLK) {
                 const int t = e / 3, v = e - 3 * (e / 3);
                 R pa[3], pb[3], wa[3], wb[3];
 #pragma unroll
@@ -731,7 +760,7 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) blocks_hybrid_
                 }
             }
         } else {
-            for (int e = threadIdx.x; e < 9 * max(na, nbt); e += BLOCK) {
+            for (int e = threadIdx.x; e < 9 * max(na, nbt); e += BS_BLK) {
                 const int t = e / 9, c = e - 9 * (e / 9);
                 if (t < na) mA[c * tris + t] = __ldg(gA + e);
                 if (t < nbt) mB[c * tris + t] = __ldg(gB + e);
@@ -742,7 +771,7 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) blocks_hybrid_
         const R eps = R(a.block_eps ? a.block_eps[blk] : a.eps_scalar);
         const BlockSource<R, T> src{a, mA, mB, tris, nbt, blk, eps};
         for (int64_t tile = 0; tile < ntile; ++tile) {
-            const int64_t p = tile * BLOCK + threadIdx.x;
+            const int64_t p = tile * BS_BLK + threadIdx.x;
             bool enq = false;
             const int i = (int)(p / nbt), k = (int)(p - (int64_t)i * nbt);
             if (p < P && !(self && i == k)) {
@@ -839,20 +868,20 @@ struct FrontierSource {
     const FrontierArgs<T>& a;
     __device__ __forceinline__ bool want_ids() const { return false; }
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
-        T* slot = thread_slot<T>(SCR * BLOCK);
+        T* slot = thread_slot<T>(SCR * BS_FRONT);
         const int64_t ia = a.fa[j], ib = a.fb[j];
         R X[9], Y[9];
         load_node(a, ia, X);
         load_node(a, ib, Y);
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-            slot[k * BLOCK] = val(X[k]);
-            slot[(9 + k) * BLOCK] = val(Y[k]);
+            slot[k * BS_FRONT] = val(X[k]);
+            slot[(9 + k) * BS_FRONT] = val(Y[k]);
         }
         A.p = slot;
-        A.stride = BLOCK;
-        B.p = slot + 9 * BLOCK;
-        B.stride = BLOCK;
+        A.stride = BS_FRONT;
+        B.p = slot + 9 * BS_FRONT;
+        B.stride = BS_FRONT;
         eps = R(T(0.5)) * (R(a.node_eps[ia]) + R(a.node_eps[ib]));
     }
     __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const {
@@ -875,9 +904,9 @@ struct FrontierSource {
 };
 
 template <typename T, bool STRICT>
-__global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) frontier_hybrid_kernel(FrontierArgs<T> a) {
+__global__ void __launch_bounds__(BS_FRONT, TC_MINB(BS_FRONT, TC_HYBRID_MINB)) frontier_hybrid_kernel(FrontierArgs<T> a) {
     using R = typename Pol<T, STRICT>::R;
-    __shared__ Queues Q;
+    __shared__ Queues<BS_FRONT> Q;
     __shared__ unsigned long long hist[32];
     const KP<R> kp = make_kp<R>(a);
     const FrontierSource<R, T> src{a};
@@ -885,26 +914,26 @@ __global__ void __launch_bounds__(BLOCK, TC_MINB(TC_HYBRID_MINB)) frontier_hybri
     if (threadIdx.x == 0) Q.n1 = Q.n2 = 0;
     if (threadIdx.x < 32) hist[threadIdx.x] = 0;
     __syncthreads();
-    const int64_t ntiles = (a.n + BLOCK - 1) / BLOCK;
+    const int64_t ntiles = (a.n + BS_FRONT - 1) / BS_FRONT;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t i = tile * BLOCK + threadIdx.x;
+        const int64_t i = tile * BS_FRONT + threadIdx.x;
         bool enq = false;
         if (i < a.n) {
             const int64_t ia = a.fa[i], ib = a.fb[i];
             R A[9], B[9];
             load_node(a, ia, A);
             load_node(a, ib, B);
-            T* slot = thread_slot<T>(SCR * BLOCK);
-            stash_pair(slot, A, B);
+            T* slot = thread_slot<T>(SCR * BS_FRONT);
+            stash_pair<BS_FRONT>(slot, A, B);
             const bool both_fine = a.is_fine[ia] && a.is_fine[ib];
             const int h = max(a.height[ia], a.height[ib]);
             atomicAdd(&hist[h < 31 ? h : 31], 1ull);
             Rec<R> r;
-            run_iterative(slot, A, B,
+            run_iterative<BS_FRONT>(slot, A, B,
                           [&] { return R(T(0.5)) * (R(a.node_eps[ia]) + R(a.node_eps[ib])); }, kp, r);
             tl.iterative++;
             if (r.kind == KIND_NOT_TERMINATED && both_fine) {
-                const SmemTri<R> SA{slot, BLOCK}, SB{slot + 9 * BLOCK, BLOCK};
+                const SmemTri<R> SA{slot, BS_FRONT}, SB{slot + 9 * BS_FRONT, BS_FRONT};
                 if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {
                     r.kind = KIND_DEGENERATE;
                     tl.degenerate++;
@@ -1057,7 +1086,7 @@ static int sm_count() {
 }
 
 template <typename K>
-static int64_t grid_for(K kernel, int64_t n, size_t smem = 0) {
+static int64_t grid_for(K kernel, int64_t n, size_t smem = 0, int threads = BLOCK) {
     if (smem > 16 * 1024) {
         // opt in to the dynamic shared memory: static + dynamic may pass the
         // 48 KB default even when the dynamic part alone does not (the call is
@@ -1065,9 +1094,9 @@ static int64_t grid_for(K kernel, int64_t n, size_t smem = 0) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, smem) != cudaSuccess || per_sm < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    const int64_t tiles = (n + BLOCK - 1) / BLOCK;
+    const int64_t tiles = (n + threads - 1) / threads;
     const int64_t full = (int64_t)sm_count() * per_sm;
     return tiles < full ? tiles : full;
 }
@@ -1091,17 +1120,18 @@ static void pool_init() {
 
 template <typename T, bool STRICT, bool SOA>
 static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
-    const size_t smem = scratch_bytes<T>();  // crossing-point scratch of the comparison phases
     if (variant == V_COMPARISON) {
         auto k = comparison_kernel<T, STRICT, SOA>;
-        k<<<(unsigned)grid_for(k, a.n, smem), BLOCK, smem, s>>>(a);
+        const size_t smem = scratch_bytes<T>(BS_CMP);  // crossing scratch + pair slot
+        k<<<(unsigned)grid_for(k, a.n, smem, BS_CMP), BS_CMP, smem, s>>>(a);
     } else if (variant == V_ITERATIVE) {
         auto k = iterative_kernel<T, STRICT, SOA>;
-        const size_t ism = sizeof(T) * 2 * SLOT * BLOCK;  // double-buffered pair slots
-        k<<<(unsigned)grid_for(k, a.n, ism), BLOCK, ism, s>>>(a);
+        const size_t smem = sizeof(T) * 2 * SLOT * BS_ITER;  // double-buffered pair slots
+        k<<<(unsigned)grid_for(k, a.n, smem, BS_ITER), BS_ITER, smem, s>>>(a);
     } else {
         auto k = hybrid_kernel<T, STRICT, SOA>;
-        k<<<(unsigned)grid_for(k, a.n, smem), BLOCK, smem, s>>>(a);
+        const size_t smem = scratch_bytes<T>(BS_HYB);
+        k<<<(unsigned)grid_for(k, a.n, smem, BS_HYB), BS_HYB, smem, s>>>(a);
     }
     g_launches++;
     const cudaError_t e = cudaGetLastError();
@@ -1151,7 +1181,7 @@ static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const int
     }
     if (nb == 0) return TC_OK;
     if (!meshes || !blocks) return TC_EINVAL;
-    const size_t smem = sizeof(T) * (SCR * BLOCK + 18 * (size_t)tris);
+    const size_t smem = sizeof(T) * (SCR * BS_BLK + 18 * (size_t)tris);
     if (smem > 200 * 1024) {
         snprintf(g_err, sizeof(g_err), "tris_per_mesh %d too large for shared-memory staging", tris);
         return TC_EINVAL;
@@ -1167,8 +1197,8 @@ static int run_blocks(const T* meshes, int32_t tris, int64_t n_meshes, const int
     a.move_factor = p->move_factor; a.start_coord = p->start_coord; a.n_iterative = p->n_iterative;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     auto launch = [&](auto k) {
-        const int64_t g = grid_for(k, nb * (int64_t)BLOCK, smem);
-        k<<<(unsigned)(g < nb ? g : nb), BLOCK, smem, s>>>(a);
+        const int64_t g = grid_for(k, nb * (int64_t)BS_BLK, smem, BS_BLK);
+        k<<<(unsigned)(g < nb ? g : nb), BS_BLK, smem, s>>>(a);
     };
     if (p->flags & TC_STRICT) launch(blocks_hybrid_kernel<T, true>);
     else launch(blocks_hybrid_kernel<T, false>);
@@ -1245,7 +1275,7 @@ static int run_multiscale(const T* tris, const int32_t* owner, const T* motions,
         cudaStreamSynchronize(s);
     }
     int64_t n = n_pairs;
-    const size_t smem = scratch_bytes<T>();
+    const size_t smem = scratch_bytes<T>(BS_FRONT);
     size_t scan_bytes = 0;
     while (n > 0) {
         if ((e = grow(n)) != cudaSuccess) return set_err("cudaMalloc", e);
@@ -1262,10 +1292,10 @@ static int run_multiscale(const T* tris, const int32_t* owner, const T* motions,
         a.move_factor = p->move_factor; a.start_coord = p->start_coord; a.n_iterative = p->n_iterative;
         if (p->flags & TC_STRICT) {
             auto k = frontier_hybrid_kernel<T, true>;
-            k<<<(unsigned)grid_for(k, n, smem), BLOCK, smem, s>>>(a);
+            k<<<(unsigned)grid_for(k, n, smem, BS_FRONT), BS_FRONT, smem, s>>>(a);
         } else {
             auto k = frontier_hybrid_kernel<T, false>;
-            k<<<(unsigned)grid_for(k, n, smem), BLOCK, smem, s>>>(a);
+            k<<<(unsigned)grid_for(k, n, smem, BS_FRONT), BS_FRONT, smem, s>>>(a);
         }
         g_launches++;
         const unsigned g = (unsigned)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
