@@ -30,10 +30,11 @@ namespace tc {
 
 // CTA sizes.  BLOCK (256) serves the one-pair-per-thread helpers and is the
 // largest CTA; the batched kernels pick their own size (measured on cfg1):
-// the iterative and all-pairs block kernels run 256-thread CTAs, the hybrid,
-// comparison and multiscale-frontier kernels 128-thread CTAs, whose queue
-// batches and per-tile barriers span half as many warps (+3 % hybrid,
-// +5 % comparison; the iterative kernel loses 3 % at 128).  Device helpers
+// the iterative and all-pairs block kernels run 256-thread CTAs, the hybrid
+// and multiscale-frontier kernels 128-thread CTAs, whose queue batches and
+// per-tile barriers span half as many warps (+3 % hybrid; 64 and 96 are
+// slower), the comparison kernel 64-thread CTAs (+7 % over 256); the
+// iterative kernel loses 3 % at 128.  Device helpers
 // read the CTA size from blockDim.x.
 constexpr int BLOCK = 256;
 #ifndef TC_BS_ITER
@@ -43,7 +44,7 @@ constexpr int BLOCK = 256;
 #define TC_BS_HYB 128
 #endif
 #ifndef TC_BS_CMP
-#define TC_BS_CMP 128
+#define TC_BS_CMP 64
 #endif
 #ifndef TC_BS_BLK
 #define TC_BS_BLK 256
