@@ -153,6 +153,9 @@ def multiscale_contacts(forest: Forest, pairs, params, *, strict=True, max_conta
             int(max_contacts), _p(idx), _p(pa), _p(pb), ctypes.byref(n_contacts), checks.ctypes.data,
             ctypes.byref(st), ctypes.c_void_p(s.cuda_stream))
     call_ms = (time.perf_counter() - t0) * 1e3
+    if rc == _abi.TC_EDEGENERATE:
+        from .kernels import DegenerateTriangle
+        raise DegenerateTriangle("degenerate triangle in comparison fallback")
     _abi.check(rc, "tc_multiscale")
     n = int(n_contacts.value)
     m = min(n, max_contacts)

@@ -85,3 +85,26 @@ def test_ragged_and_self_blocks_counts():
     PT.blocks_hybrid(torch.from_numpy(meshes).cuda(), blocks, D.Params(), mesh_tris=cnt, stats=st)
     s = D.read_stats(st)
     assert s["iterative"] == 50 * 17 + 17 * 33 + 33 * 32 + 17 * 16
+
+
+@pytest.mark.parametrize("same", [False, True])
+def test_find_contacts_chunked_path_equals_block_path(monkeypatch, same):
+    # soups beyond the shared-memory staging limit go through kernels.hybrid_batch
+    # in chunks (like the reference); both paths must give the same contacts
+    g = load("float64")
+    ti = g["fc_two_tris_i"].reshape(-1, 3, 3)
+    tj = ti if same else g["fc_two_tris_j"].reshape(-1, 3, 3)
+    c1 = K.KernelCounters()
+    block = C.find_contacts_single_level(ti, tj, K.KernelParams(), c1)
+    monkeypatch.setitem(C._STAGE_LIMIT, np.dtype(np.float64), 8)
+    c2 = K.KernelCounters()
+    chunked = C.find_contacts_single_level(ti, tj, K.KernelParams(), c2, chunk=1000)
+    assert [c.source for c in block] == [c.source for c in chunked]
+    assert all(a.position.tobytes() == b.position.tobytes() for a, b in zip(block, chunked))
+    assert c1.as_dict() == c2.as_dict()
+    if same:
+        assert all(s0 != s1 for s0, s1 in (c.source for c in chunked))
+
+
+def test_find_contacts_empty_soup():
+    assert C.find_contacts_single_level(np.zeros((0, 3, 3)), np.ones((3, 3, 3))) == []

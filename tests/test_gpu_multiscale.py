@@ -145,3 +145,21 @@ def test_fused_motion_matches_reference(real):
             res_w, cp_w = _run(wt, pairs, dt, strict=False)
             assert np.array_equal(cp["source"], cp_w["source"])
             assert cp["position"].tobytes() == cp_w["position"].tobytes()
+
+
+def test_degenerate_mesh_triangle_raises():
+    # a mesh-level fallback pair with a degenerate triangle: the reference
+    # raises DegenerateTriangle (RK/kernels.py:598-600); the traversal returns
+    # TC_EDEGENERATE, which the wrapper raises
+    from paper_2105_12415_b200 import kernels
+
+    g = load("float64")
+    sc = "s80_rest"
+    ti, tj = tree(g, sc, "i"), tree(g, sc, "j")
+    tris = ti["tris"].reshape(-1, 3, 3).copy()
+    # collapse every mesh triangle of particle i onto a line
+    fine = np.arange(ti["n_nodes"], tris.shape[0])
+    tris[fine, 2] = tris[fine, 0] + 2.0 * (tris[fine, 1] - tris[fine, 0])
+    ti = dict(ti, tris=tris.reshape(-1, 9))
+    with pytest.raises(kernels.DegenerateTriangle):
+        _run([ti, tj], [(0, 1)], np.float64)
