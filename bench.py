@@ -116,6 +116,16 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_rate(seconds: float, chunk: int, threads: int, start: int = 0):
     """Time the oracle port's hybrid on consecutive chunks until `seconds` pass."""
     sys.path.insert(0, str(ROOT / "oracle"))
@@ -163,7 +173,8 @@ def run_reference(args, rank):
                    "pairs_per_step": sample, "layout": "(n,3,3) host"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{sample} pairs of the cfg1 generator per step (oracle/tc_oracle.c, "
-                                   "C restatement of RK/kernels.py, bit-identical to the reference)"},
+                                   "C restatement of RK/kernels.py, bit-identical to the reference)",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -355,9 +366,13 @@ def main():
         if rank == 0 and world == 1:
             threads = len(os.sched_getaffinity(0))
             rate, done = cpu_oracle_rate(10.0, 1 << 17, threads)
+            rate1, done1 = cpu_oracle_rate(3.0, 1 << 14, 1)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                                     "sample": f"{done} pairs of the cfg1 generator in 131072-pair chunks, hybrid "
-                                              "(16, 1e-6), oracle/tc_oracle.c on all host threads"}
+                                              "(16, 1e-6), oracle/tc_oracle.c on all host threads; generation "
+                                              "excluded",
+                                    "one_core": {"value": rate1, "sample": f"{done1} pairs, 1 thread"},
+                                    "cpu_model": cpu_model()}
             line["variants"] = variant_table(D, torch, A[: 1 << 22], B[: 1 << 22], dev)
             line["configs"] = configs_table(D, torch, dev)
     if rank == 0:
