@@ -70,7 +70,13 @@ def contact_from_segment_batch(point_a: np.ndarray, point_b: np.ndarray, eps_a, 
     w = np.broadcast_to(ea / (ea + eb), (point_a.shape[0],)).astype(real)
     position = point_a + w[:, None] * (point_b - point_a)
     normal = point_a - position
-    small = np.array([np.linalg.norm(v) < 1e-12 for v in normal], bool)
+    # |normal| < 1e-12, decided like the reference's per-contact
+    # np.linalg.norm; only rows within rounding of the threshold need it
+    n2 = np.einsum("ij,ij->i", normal.astype(np.float64), normal.astype(np.float64))
+    small = n2 < 1e-24
+    near = np.nonzero(np.abs(n2 - 1e-24) <= 1e-30)[0]
+    for k in near:
+        small[k] = np.linalg.norm(normal[k]) < 1e-12
     normal[small] = 0.0
     return position, normal
 

@@ -159,12 +159,16 @@ def multiscale_contacts(forest: Forest, pairs, params, *, strict=True, max_conta
     _abi.check(rc, "tc_multiscale")
     n = int(n_contacts.value)
     m = min(n, max_contacts)
-    ih = idx[:m].cpu().numpy()
-    order = np.lexsort((ih[:, 2], ih[:, 1], ih[:, 0]))
+    # order by (pair, id_i, id_j) on the device: three stable sorts, last key first
+    d_idx = idx[:m]
+    perm = torch.arange(m, device=dev)
+    for col in (2, 1, 0):
+        perm = perm[torch.sort(d_idx[perm, col], stable=True).indices]
+    ih = d_idx[perm].cpu().numpy()
     stats = {k: getattr(st, k) for k in ("iterative", "comparison", "fallback", "degenerate", "contacts",
                                          "intersecting", "min_distance")}
-    return MultiscaleResult(n, ih[order, 0], ih[order, 1], ih[order, 2], pa[:m].cpu().numpy()[order],
-                            pb[:m].cpu().numpy()[order], checks, stats, call_ms)
+    return MultiscaleResult(n, ih[:, 0], ih[:, 1], ih[:, 2], pa[:m][perm].cpu().numpy(),
+                            pb[:m][perm].cpu().numpy(), checks, stats, call_ms)
 
 
 def contact_points(forest: Forest, res: MultiscaleResult, pairs):
