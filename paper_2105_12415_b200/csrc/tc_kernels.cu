@@ -1,16 +1,24 @@
 // tc_kernels.cu -- sm_100a kernels and the C ABI of include/tricontact_b200.h.
 //
 // Kernels (one triangle pair per thread, grid-stride / persistent over the
-// pair range, grid sized to the SM count x resident CTAs per SM):
+// pair range, grid sized to the SM count x resident CTAs per SM; CTA sizes
+// per kernel, see BS_* below):
 //   comparison_kernel  RK/kernels.py:301-401
-//   iterative_kernel   RK/kernels.py:447-565
-//   hybrid_kernel      RK/kernels.py:568-605 -- iterative for a tile of
-//       BLOCK pairs, NOT_TERMINATED lanes (with allow_fb) are appended to a
-//       shared-memory queue by warp ballot; whenever the queue holds a full
-//       block of pairs, all BLOCK threads run the comparison kernel on it, so
-//       the divergent fallback executes on full warps.  The fallback never
+//   iterative_kernel   RK/kernels.py:447-565 (pairs double-buffered in
+//       shared memory by cp.async one tile ahead)
+//   hybrid_kernel      RK/kernels.py:568-605 -- iterative for a tile of one
+//       pair per thread, NOT_TERMINATED lanes (with allow_fb) are appended to
+//       a shared-memory queue by warp ballot; whenever the queue holds a full
+//       CTA of pairs, all threads run the comparison phases on it, so the
+//       divergent fallback executes on full warps.  The fallback never
 //       leaves the kernel.
-//   cpt_kernel / degenerate_kernel: RK/kernels.py:157, RK/geometry.py:68.
+//   blocks_hybrid_kernel  all-pairs particle blocks (RK/stepping.py:285-308,
+//       RK/contact.py:97-140): both meshes staged in shared memory, optional
+//       fused rigid motions (RK/geometry.py:162-176)
+//   frontier_hybrid_kernel + frontier_count/write_kernel  the multiscale
+//       traversal's rounds (RK/stepping.py:311-368)
+//   cpt_kernel / ptd_kernel / degenerate_kernel: RK/kernels.py:157,
+//       RK/surrogate.py:237-257, RK/geometry.py:68.
 // Every kernel reduces its tallies per CTA (warp shuffles) and folds them
 // into a device tc_stats with one set of atomics per CTA.
 #include <cuda_runtime.h>
