@@ -192,27 +192,15 @@ __device__ __forceinline__ void run_iterative(const TA& SA, const TB& SB, const 
             }
         });
     } else {
-        auto reload = [&](R* A0, R* B0, R* E0, R* E1, R* E3, R* E4, R* sq, R* eps_out) {
+        auto reload = [&](R* A9, R* B9) {
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const R a0 = SA[k], b0 = SB[k];
-                A0[k] = a0;
-                B0[k] = b0;
-                E0[k] = SA[3 + k] - a0;
-                E1[k] = SA[6 + k] - a0;
-                E3[k] = b0 - SB[3 + k];
-                E4[k] = b0 - SB[6 + k];
-            }
-            if (sq) {
-                R ta[9], tb[9];
-#pragma unroll
-                for (int k = 0; k < 9; ++k) { ta[k] = SA[k]; tb[k] = SB[k]; }
-                *sq = maxv(max_sq_edge(ta), max_sq_edge(tb));
-                *eps_out = eps_fn();
+            for (int k = 0; k < 9; ++k) {
+                A9[k] = SA[k];
+                B9[k] = SB[k];
             }
         };
-        if (kp.start_coord >= R(0) && kp.start_coord <= R(1)) iterative_pair_gram<true>(A, B, kp, r, reload);
-        else iterative_pair_gram<false>(A, B, kp, r, reload);
+        if (kp.start_coord >= R(0) && kp.start_coord <= R(1)) iterative_pair_gram<true>(A, B, kp, r, reload, eps_fn);
+        else iterative_pair_gram<false>(A, B, kp, r, reload, eps_fn);
     }
 }
 template <int BS, class R, typename T, class EpsFn>

@@ -763,6 +763,13 @@ struct GramSolver {
     R x0, x1, x2, x3;
     R g0, g1, g3, g4;
 
+    // Setup.  The slide directions' products come from the Gram matrix
+    // (e3a = E1 - E0: SA_k = G1k - G0k; -e3b = E4 - E3: SB_k = G4k - G3k);
+    // their squared lengths are dotted directly (they set the slide step
+    // size).  _pair_max_sq_edge (RK/kernels.py:409-414) is the max over the
+    // six squared edges G00, G11, |e3a|^2, G33, G44, |e3b|^2, and the TINY
+    // floor of the denominators (RK/kernels.py:490) is applied once to the
+    // regulariser (equal unless alpha_reg * sq < 1e-30).
     __device__ __forceinline__ void init(const R* A, const R* B, const KP<R>& kp) {
         const R tiny = R(Tiny<R>::v);
         x0 = x1 = x2 = x3 = kp.start_coord;
@@ -779,16 +786,17 @@ struct GramSolver {
         G00 = dot3(E0, E0); G01 = dot3(E0, E1); G03 = dot3(E0, E3); G04 = dot3(E0, E4);
         G11 = dot3(E1, E1); G13 = dot3(E1, E3); G14 = dot3(E1, E4);
         G33 = dot3(E3, E3); G34 = dot3(E3, E4); G44 = dot3(E4, E4);
-        SA0 = dot3(SA, E0); SA1 = dot3(SA, E1); SA3 = dot3(SA, E3); SA4 = dot3(SA, E4);
-        SB0 = dot3(SB, E0); SB1 = dot3(SB, E1); SB3 = dot3(SB, E3); SB4 = dot3(SB, E4);
-        const R sq = maxv(max_sq_edge(A), max_sq_edge(B));
-        const R alpha_reg = kp.alpha_reg * sq;
-        r0 = rcpv(maxv(G00 + alpha_reg, tiny));
-        r1 = rcpv(maxv(G11 + alpha_reg, tiny));
-        r2 = rcpv(maxv(G33 + alpha_reg, tiny));
-        r3 = rcpv(maxv(G44 + alpha_reg, tiny));
-        r3a = rcpv(maxv(dot3(SA, SA) + alpha_reg, tiny));
-        r3b = rcpv(maxv(dot3(SB, SB) + alpha_reg, tiny));
+        SA0 = G01 - G00; SA1 = G11 - G01; SA3 = G13 - G03; SA4 = G14 - G04;
+        SB0 = G04 - G03; SB1 = G14 - G13; SB3 = G34 - G33; SB4 = G44 - G34;
+        const R qa = dot3(SA, SA), qb = dot3(SB, SB);
+        const R sq = maxv(maxv(maxv(G00, G11), qa), maxv(maxv(G33, G44), qb));
+        const R areg = maxv(kp.alpha_reg * sq, tiny);
+        r0 = rcpv(G00 + areg);
+        r1 = rcpv(G11 + areg);
+        r2 = rcpv(G33 + areg);
+        r3 = rcpv(G44 + areg);
+        r3a = rcpv(qa + areg);
+        r3b = rcpv(qb + areg);
 #pragma unroll
         for (int i = 0; i < 3; ++i) d[i] = (A[i] - B[i]) + x0 * E0[i] + x1 * E1[i] + x2 * E3[i] + x3 * E4[i];
         g0 = dot3(d, E0); g1 = dot3(d, E1); g3 = dot3(d, E3); g4 = dot3(d, E4);
@@ -822,67 +830,105 @@ struct GramSolver {
         g0 += t * SB0; g1 += t * SB1; g3 += t * SB3; g4 += t * SB4;
     }
 
-    // epilogue: re-read the pair (shared-memory copy) and rebuild d exactly
-    // from x, once before the last sweep (prelast) and once after (finish),
-    // so nothing but x, g and the Gram terms is live across a sweep; the
-    // penalty weight and the halo are re-derived rather than kept live.
-    struct Pre { R j_old, mid_old[3], alpha_it, eps; };
+    // Epilogue.  The pair is re-read (shared-memory copy) where needed, so
+    // nothing but x, g and the Gram terms is live across a sweep.  Both
+    // points come from the barycentric weights, pa = (1 - x0 - x1) A0 +
+    // x0 A1 + x1 A2 (likewise pb), d = pa - pb, and the contact midpoint
+    // A0 + x0 e1a + x1 e2a - d/2 of RK/kernels.py:521,548 is (pa + pb) / 2,
+    // so the move between the last two sweeps is |S - S_old| / 2 with
+    // S = pa + pb (tested squared: |S - S_old|^2 <= 4 (mf eps)^2).  The penalty weight re-derives _pair_max_sq_edge from the
+    // Gram terms (|e3a|^2 = SA1 - SA0, |e3b|^2 = SB4 - SB3).
+    struct Pre { R j_old, s_old[3], eps, alpha_it; };
+
+    __device__ __forceinline__ R alpha_it(const KP<R>& kp) const {
+        const R sq = maxv(maxv(maxv(G00, G11), SA1 - SA0), maxv(maxv(G33, G44), SB4 - SB3));
+        return kp.alpha_it * sq;
+    }
+
+    // RK/kernels.py:417-431; in BOX mode the iterates satisfy x >= 0 exactly
+    // (clips and slides never produce a negative coordinate), so the four
+    // max(0, -x) terms vanish
+    __device__ __forceinline__ R penalty_x(R alpha) const {
+        if (!BOX) {
+            const R xs[4] = {x0, x1, x2, x3};
+            return penalty(xs, alpha);
+        }
+        const R z = R(0), one = R(1);
+        R p = maxv(z, x0 - one) + maxv(z, x1 - one);
+        p = p + maxv(z, (x0 + x1) - one);
+        p = p + (maxv(z, x2 - one) + maxv(z, x3 - one));
+        p = p + maxv(z, (x2 + x3) - one);
+        return alpha * p;
+    }
 
     template <class Reload>
-    __device__ __forceinline__ void prelast(Reload& reload, const KP<R>& kp, Pre& pre) const {
-        using T = typename Store<R>::type;
-        R A0[3], B0[3], E0[3], E1[3], E3[3], E4[3], d[3], sq;
-        reload(A0, B0, E0, E1, E3, E4, &sq, &pre.eps);
-        pre.alpha_it = kp.alpha_it * sq;
+    __device__ __forceinline__ void points(Reload& reload, R* pa, R* pb) const {
+        R A[9], B[9];
+        reload(A, B);
+        const R wa = (R(1) - x0) - x1, wb = (R(1) - x2) - x3;
 #pragma unroll
-        for (int i = 0; i < 3; ++i) d[i] = (A0[i] - B0[i]) + x0 * E0[i] + x1 * E1[i] + x2 * E3[i] + x3 * E4[i];
-        const R xs[4] = {x0, x1, x2, x3};
-        pre.j_old = R(T(0.5)) * dot3(d, d) + penalty(xs, pre.alpha_it);
-        contact_mid(A0, xs, E0, E1, d, pre.mid_old);
+        for (int i = 0; i < 3; ++i) {
+            pa[i] = (wa * A[i] + x0 * A[3 + i]) + x1 * A[6 + i];
+            pb[i] = (wb * B[i] + x2 * B[3 + i]) + x3 * B[6 + i];
+        }
+    }
+
+    template <class Reload, class EpsFn>
+    __device__ __forceinline__ void prelast(Reload& reload, EpsFn& eps_fn, const KP<R>& kp, Pre& pre) const {
+        R pa[3], pb[3], d[3];
+        points(reload, pa, pb);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            d[i] = pa[i] - pb[i];
+            pre.s_old[i] = pa[i] + pb[i];
+        }
+        pre.alpha_it = alpha_it(kp);
+        pre.j_old = R(typename Store<R>::type(0.5)) * dot3(d, d) + penalty_x(pre.alpha_it);
+        pre.eps = eps_fn();
     }
 
     template <class Reload>
     __device__ __forceinline__ void finish(Reload& reload, const KP<R>& kp, const Pre& pre, Rec<R>& o) const {
         using T = typename Store<R>::type;
         const R half = R(T(0.5));
-        R A0[3], B0[3], E0[3], E1[3], E3[3], E4[3], d[3];
-        reload(A0, B0, E0, E1, E3, E4, nullptr, nullptr);
+        R pa[3], pb[3], d[3], mv[3];
+        points(reload, pa, pb);
 #pragma unroll
-        for (int i = 0; i < 3; ++i) d[i] = (A0[i] - B0[i]) + x0 * E0[i] + x1 * E1[i] + x2 * E3[i] + x3 * E4[i];
-        const R xs[4] = {x0, x1, x2, x3};
+        for (int i = 0; i < 3; ++i) {
+            d[i] = pa[i] - pb[i];
+            mv[i] = (pa[i] + pb[i]) - pre.s_old[i];
+        }
         const R dd = dot3(d, d);
-        const R j_total = half * dd + penalty(xs, pre.alpha_it);
-        R mv[3];
-        contact_mid(A0, xs, E0, E1, d, mv);
-#pragma unroll
-        for (int i = 0; i < 3; ++i) mv[i] = mv[i] - pre.mid_old[i];
-        const R move = sqrtv(norm3_sq_sum(mv));
         const R jh = half * dd;
+        const R j_total = jh + penalty_x(pre.alpha_it);
         const R eps = pre.eps;
-        const bool settled = (absv(j_total - pre.j_old) <= kp.c_factor * eps) && (move <= kp.move_factor * eps);
+        // move = |S - S_old| / 2 <= mf * eps, compared squared (no sqrt)
+        const R mlim = kp.move_factor * eps;
+        const bool settled = (absv(j_total - pre.j_old) <= kp.c_factor * eps) &&
+                             (dot3(mv, mv) <= R(typename Store<R>::type(4)) * (mlim * mlim));
         const bool contact = settled && (jh <= (R(T(2)) * eps) * eps);
         o.kind = contact ? KIND_CONTACT : (settled ? KIND_NO_CONTACT : KIND_NOT_TERMINATED);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            o.pa[i] = (A0[i] + x0 * E0[i]) + x1 * E1[i];
-            o.pb[i] = (B0[i] - x2 * E3[i]) - x3 * E4[i];
+            o.pa[i] = pa[i];
+            o.pb[i] = pb[i];
         }
-        o.distance = sqrtv(R(T(2)) * jh);
+        o.distance = sqrtv(dd);   // sqrt(2 * jh): halving and doubling are exact
         o.ba[0] = x0; o.ba[1] = x1;
         o.bb[0] = x2; o.bb[1] = x3;
         o.ids = 0x00FFFFFFu | ((uint32_t)((settled ? FLAG_SETTLED : 0u) | (contact ? FLAG_ITER_CONTACT : 0u)) << 24);
     }
 };
 
-template <bool BOX, class R, class Reload>
+template <bool BOX, class R, class Reload, class EpsFn>
 __device__ __forceinline__ void iterative_pair_gram(const R* A, const R* B, const KP<R>& kp, Rec<R>& o,
-                                                    Reload reload) {
+                                                    Reload reload, EpsFn eps_fn) {
     GramSolver<BOX, R> gs;
     gs.init(A, B, kp);
 #pragma unroll 1
     for (int it = 0; it < kp.n_iterative - 1; ++it) gs.sweep();
     typename GramSolver<BOX, R>::Pre pre;
-    gs.prelast(reload, kp, pre);
+    gs.prelast(reload, eps_fn, kp, pre);
     gs.sweep();
     gs.finish(reload, kp, pre, o);
 }
