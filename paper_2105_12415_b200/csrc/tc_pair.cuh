@@ -89,23 +89,9 @@ __device__ __forceinline__ bool degenerate_tri(const R* t) {
 // denominator, so the divergent region cases cost one division pair for the
 // whole warp.  u, w are the weights along ab, ac; results are the
 // reference's bit for bit in strict mode.
-template <class R, class Tri>
-__device__ __forceinline__ int closest_point_params_t(const R* p, const Tri& tri, R& u, R& w) {
-    R a[3], b[3], c[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) { a[i] = tri[i]; b[i] = tri[3 + i]; c[i] = tri[6 + i]; }
-    R ab[3], ac[3], t3[3];
-    sub3(b, a, ab);
-    sub3(c, a, ac);
-    sub3(p, a, t3);
-    const R d1 = dot3(ab, t3);
-    const R d2 = dot3(ac, t3);
-    sub3(p, b, t3);
-    const R d3 = dot3(ab, t3);
-    const R d4 = dot3(ac, t3);
-    sub3(p, c, t3);
-    const R d5 = dot3(ab, t3);
-    const R d6 = dot3(ac, t3);
+// Region and weights from the six dot products d1..d6 (RK/kernels.py:180-218).
+template <class R>
+__device__ __forceinline__ int region_params(R d1, R d2, R d3, R d4, R d5, R d6, R& u, R& w) {
     const R vc = d1 * d4 - d3 * d2;
     const R vb = d5 * d2 - d1 * d6;
     const R va = d3 * d6 - d5 * d4;
@@ -134,6 +120,61 @@ __device__ __forceinline__ int closest_point_params_t(const R* p, const Tri& tri
     if (region == 4) w = q1;
     if (region == 5) { u = R(1) - q1; w = q1; }
     if (region == 6) { u = q1; w = divv(vc, den); }
+    return region;
+}
+
+template <class R, class Tri>
+__device__ __forceinline__ int closest_point_params_t(const R* p, const Tri& tri, R& u, R& w) {
+    R a[3], b[3], c[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) { a[i] = tri[i]; b[i] = tri[3 + i]; c[i] = tri[6 + i]; }
+    R ab[3], ac[3], t3[3];
+    sub3(b, a, ab);
+    sub3(c, a, ac);
+    sub3(p, a, t3);
+    const R d1 = dot3(ab, t3);
+    const R d2 = dot3(ac, t3);
+    sub3(p, b, t3);
+    const R d3 = dot3(ab, t3);
+    const R d4 = dot3(ac, t3);
+    sub3(p, c, t3);
+    const R d5 = dot3(ab, t3);
+    const R d6 = dot3(ac, t3);
+    return region_params(d1, d2, d3, d4, d5, d6, u, w);
+}
+
+// Fast build: the target triangle's frame (origin, edges ab, ac and their
+// Gram terms), shared by the three point tests against it.  With ap = p - a:
+// d3 = d1 - ab.ab, d4 = d2 - ab.ac, d5 = d1 - ab.ac, d6 = d2 - ac.ac, and
+// the offset to the closest point is ap - u ab - w ac, which also gives the
+// squared distance.  Equal to the reference's d1..d6 and distance up to
+// rounding (the winner's points are rebuilt with the reference's formulas).
+template <class R>
+struct PointFrame {
+    R a[3], ab[3], ac[3], gbb, gbc, gcc;
+};
+template <class R, class Tri>
+__device__ __forceinline__ void point_frame(const Tri& tri, PointFrame<R>& f) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        f.a[i] = tri[i];
+        f.ab[i] = tri[3 + i] - f.a[i];
+        f.ac[i] = tri[6 + i] - f.a[i];
+    }
+    f.gbb = dot3(f.ab, f.ab);
+    f.gbc = dot3(f.ab, f.ac);
+    f.gcc = dot3(f.ac, f.ac);
+}
+template <class R>
+__device__ __forceinline__ int closest_point_frame(const R* p, const PointFrame<R>& f, R& u, R& w, R& dist2) {
+    R ap[3];
+    sub3(p, f.a, ap);
+    const R d1 = dot3(f.ab, ap), d2 = dot3(f.ac, ap);
+    const int region = region_params(d1, d2, d1 - f.gbb, d2 - f.gbc, d1 - f.gbc, d2 - f.gcc, u, w);
+    R diff[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) diff[i] = (ap[i] - u * f.ab[i]) - w * f.ac[i];
+    dist2 = dot3(diff, diff);
     return region;
 }
 
@@ -212,16 +253,20 @@ __device__ __forceinline__ int closest_point_triangle(const R* p, const R* tri, 
 // and re = 1/e are the hoisted reciprocals of the two squared edge lengths
 // (with the reference's TINY guard applied).  Branch code: bit0 = s from the
 // 2x2 solve, bit1 = t < 0, bit2 = t > 1.
+//
+// la / le: the hoisted squared edge lengths (the fast build uses them
+// instead of re-dotting; the same values), and the fast build takes the
+// offset of the two closest points as r + s d1 - t d2.
 template <class R>
 __device__ __forceinline__ int segment_params(const R* p1, const R* q1, const R* p2, const R* q2, R ra, R re,
-                                              R& s, R& t, R& d2out) {
+                                              R la, R le, R& s, R& t, R& d2out) {
     const R tiny = R(Tiny<R>::v);
     R d1[3], d2[3], r[3];
     sub3(q1, p1, d1);
     sub3(q2, p2, d2);
     sub3(p1, p2, r);
-    const R a = dot3(d1, d1);
-    const R e = dot3(d2, d2);
+    const R a = IsStrict<R>::value ? dot3(d1, d1) : la;
+    const R e = IsStrict<R>::value ? dot3(d2, d2) : le;
     const R f = dot3(d2, r);
     const R c = dot3(d1, r);
     const R b = dot3(d1, d2);
@@ -238,7 +283,8 @@ __device__ __forceinline__ int segment_params(const R* p1, const R* q1, const R*
     t = clipv(t, R(0), R(1));
     R diff[3];
 #pragma unroll
-    for (int i = 0; i < 3; ++i) diff[i] = (p1[i] + s * d1[i]) - (p2[i] + t * d2[i]);
+    for (int i = 0; i < 3; ++i)
+        diff[i] = IsStrict<R>::value ? (p1[i] + s * d1[i]) - (p2[i] + t * d2[i]) : (r[i] + s * d1[i]) - t * d2[i];
     d2out = dot3(diff, diff);
     return (solve ? 1 : 0) | (lo ? 2 : 0) | (hi ? 4 : 0);
 }
@@ -432,41 +478,61 @@ __device__ __forceinline__ void comparison_phase2_impl(const Tri& A, const Tri& 
     R best = R(0), bp1 = R(0), bp2 = R(0);
     // (two loops with fixed source/target triangles: a runtime choice between
     // the A and B arrays would force them out of registers)
+    if constexpr (IsStrict<R>::value) {
 #pragma unroll kUnrollF
-    for (int row = 0; row < 3; ++row) {
-        R pt[3], u, w, cl[3], diff[3];
-        A.vertex(row, pt);
-        const int reg = closest_point_params_t(pt, B, u, w);
-        bary_point_t(B, u, w, cl);
-        sub3(pt, cl, diff);
-        const R d2 = dot3(diff, diff);
-        if (row == 0 || d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
-    }
+        for (int row = 0; row < 3; ++row) {
+            R pt[3], u, w, cl[3], diff[3];
+            A.vertex(row, pt);
+            const int reg = closest_point_params_t(pt, B, u, w);
+            bary_point_t(B, u, w, cl);
+            sub3(pt, cl, diff);
+            const R d2 = dot3(diff, diff);
+            if (row == 0 || d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
+        }
 #pragma unroll kUnrollF
-    for (int row = 3; row < 6; ++row) {
-        R pt[3], u, w, cl[3], diff[3];
-        B.vertex(row - 3, pt);
-        const int reg = closest_point_params_t(pt, A, u, w);
-        bary_point_t(A, u, w, cl);
-        sub3(pt, cl, diff);
-        const R d2 = dot3(diff, diff);
-        if (d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
+        for (int row = 3; row < 6; ++row) {
+            R pt[3], u, w, cl[3], diff[3];
+            B.vertex(row - 3, pt);
+            const int reg = closest_point_params_t(pt, A, u, w);
+            bary_point_t(A, u, w, cl);
+            sub3(pt, cl, diff);
+            const R d2 = dot3(diff, diff);
+            if (d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
+        }
+    } else {
+        PointFrame<R> f;
+        point_frame(B, f);
+#pragma unroll kUnrollF
+        for (int row = 0; row < 3; ++row) {
+            R pt[3], u, w, d2;
+            A.vertex(row, pt);
+            const int reg = closest_point_frame(pt, f, u, w, d2);
+            if (row == 0 || d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
+        }
+        point_frame(A, f);
+#pragma unroll kUnrollF
+        for (int row = 3; row < 6; ++row) {
+            R pt[3], u, w, d2;
+            B.vertex(row - 3, pt);
+            const int reg = closest_point_frame(pt, f, u, w, d2);
+            if (d2 < best) { best = d2; best_row = row; best_code = reg; bp1 = u; bp2 = w; }
+        }
     }
-    // hoisted reciprocals of the six squared edge lengths (TINY-guarded)
-    R ra[3], rb[3];
+    // hoisted squared edge lengths and their reciprocals (TINY-guarded)
+    R la[3], lb[3], ra[3], rb[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         R p[3], q[3], d[3];
         A.vertex(edge_start(k), p);
         A.vertex(edge_end(k), q);
         sub3(q, p, d);
-        R l = dot3(d, d);
-        ra[k] = rcpv(l > tiny ? l : R(1));
+        la[k] = dot3(d, d);
+        ra[k] = rcpv(la[k] > tiny ? la[k] : R(1));
         B.vertex(edge_start(k), p);
         B.vertex(edge_end(k), q);
         sub3(q, p, d);
-        l = dot3(d, d);
-        rb[k] = rcpv(l > tiny ? l : R(1));
+        lb[k] = dot3(d, d);
+        rb[k] = rcpv(lb[k] > tiny ? lb[k] : R(1));
     }
 #pragma unroll kUnrollF
     for (int row = 6; row < 15; ++row) {
@@ -478,7 +544,9 @@ __device__ __forceinline__ void comparison_phase2_impl(const Tri& A, const Tri& 
         B.vertex(edge_end(kb), q2);
         const R rak = (ka == 0) ? ra[0] : ((ka == 1) ? ra[1] : ra[2]);
         const R rbk = (kb == 0) ? rb[0] : ((kb == 1) ? rb[1] : rb[2]);
-        const int code = segment_params(p1, q1, p2, q2, rak, rbk, s, t, d2);
+        const R lak = (ka == 0) ? la[0] : ((ka == 1) ? la[1] : la[2]);
+        const R lbk = (kb == 0) ? lb[0] : ((kb == 1) ? lb[1] : lb[2]);
+        const int code = segment_params(p1, q1, p2, q2, rak, rbk, lak, lbk, s, t, d2);
         if (d2 < best) { best = d2; best_row = row; best_code = code; bp1 = s; bp2 = t; }
     }
     o.ids = (uint32_t)best_row | ((uint32_t)best_code << 8);
