@@ -242,3 +242,32 @@ def test_fast_vs_oracle_one_million(oracle_lib, real):
     got, _ = run_dev("hybrid", A, B, real, "bl", False)
     rep = parity.compare_fast(oracle_lib, "hybrid", A, B, PARAM_SETS["bl"], got, dt)
     assert rep["ok"], str(rep)
+
+
+# ---------------------------------------------------------------------------
+# start_coord outside [0, 1] (KernelParams allows any value): the fast build
+# then runs the general clips (no box shortcut) and the full penalty; strict
+# stays bit-identical.
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("start", [-0.25, 0.0, 1.0, 1.5])
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_start_coord_general(oracle_lib, real, start):
+    dt = DTYPES[real]
+    A, B = W.random_pairs(1 << 13, seed=0, sep=(-0.1, 0.5), start=1 << 16)
+    A = A.astype(dt)
+    B = B.astype(dt)
+    pk = dict(n_iterative=16, epsilon=1e-6, start_coord=start)
+    ta, tb = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    ref, counts, rc = oracle_lib.hybrid(A, B, oracle_lib.make_params(**pk), pk["epsilon"], dtype=dt)
+    assert rc == 0
+    for variant in ("iterative", "hybrid"):
+        strict = D.run(variant, ta, tb, D.Params(**pk), strict=True, ids=True)
+        fast = D.run(variant, ta, tb, D.Params(**pk), strict=False, ids=True)
+        torch.cuda.synchronize()
+        got = {k: v.cpu().numpy() for k, v in fast.items()}
+        rep = parity.compare_fast(oracle_lib, variant, A, B, pk, got, dt)
+        assert rep["ok"], (variant, str(rep))
+        if variant == "hybrid":
+            for k in COLS:
+                assert np.array_equal(strict[k].cpu().numpy(), ref[k]), k
