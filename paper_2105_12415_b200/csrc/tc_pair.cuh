@@ -913,20 +913,15 @@ struct GramSolver {
         return kp.alpha_it * sq;
     }
 
-    // RK/kernels.py:417-431; in BOX mode the iterates satisfy x >= 0 exactly
-    // (clips and slides never produce a negative coordinate), so the four
-    // max(0, -x) terms vanish
+    // RK/kernels.py:417-431.  In BOX mode the iterates satisfy x >= 0 exactly
+    // (clips and slides never produce a negative coordinate) and x <= 1,
+    // x_a + x_b <= 1 up to a few ulps (each clip bounds a coordinate by
+    // 1 - partner), so the penalty is 0 or alpha * O(ulp): below the
+    // resolution of the settle test, and it is dropped.
     __device__ __forceinline__ R penalty_x(R alpha) const {
-        if (!BOX) {
-            const R xs[4] = {x0, x1, x2, x3};
-            return penalty(xs, alpha);
-        }
-        const R z = R(0), one = R(1);
-        R p = maxv(z, x0 - one) + maxv(z, x1 - one);
-        p = p + maxv(z, (x0 + x1) - one);
-        p = p + (maxv(z, x2 - one) + maxv(z, x3 - one));
-        p = p + maxv(z, (x2 + x3) - one);
-        return alpha * p;
+        if (BOX) return R(0);
+        const R xs[4] = {x0, x1, x2, x3};
+        return penalty(xs, alpha);
     }
 
     template <class Reload>
@@ -950,7 +945,7 @@ struct GramSolver {
             d[i] = pa[i] - pb[i];
             pre.s_old[i] = pa[i] + pb[i];
         }
-        pre.alpha_it = alpha_it(kp);
+        pre.alpha_it = BOX ? R(0) : alpha_it(kp);
         pre.j_old = R(typename Store<R>::type(0.5)) * dot3(d, d) + penalty_x(pre.alpha_it);
         pre.eps = eps_fn();
     }
