@@ -906,7 +906,7 @@ struct GramSolver {
     // so the move between the last two sweeps is |S - S_old| / 2 with
     // S = pa + pb (tested squared: |S - S_old|^2 <= 4 (mf eps)^2).  The penalty weight re-derives _pair_max_sq_edge from the
     // Gram terms (|e3a|^2 = SA1 - SA0, |e3b|^2 = SB4 - SB3).
-    struct Pre { R j_old, s_old[3], eps, alpha_it; };
+    struct Pre { R x_old[4], j_old, s_old[3], eps, alpha_it; };
 
     __device__ __forceinline__ R alpha_it(const KP<R>& kp) const {
         const R sq = maxv(maxv(maxv(G00, G11), SA1 - SA0), maxv(maxv(G33, G44), SB4 - SB3));
@@ -938,6 +938,9 @@ struct GramSolver {
 
     template <class Reload, class EpsFn>
     __device__ __forceinline__ void prelast(Reload& reload, EpsFn& eps_fn, const KP<R>& kp, Pre& pre) const {
+        pre.eps = eps_fn();
+        pre.x_old[0] = x0; pre.x_old[1] = x1; pre.x_old[2] = x2; pre.x_old[3] = x3;
+        if (BOX) return;   // finish() works from the last sweep's dx and the Gram terms
         R pa[3], pb[3], d[3];
         points(reload, pa, pb);
 #pragma unroll
@@ -945,30 +948,48 @@ struct GramSolver {
             d[i] = pa[i] - pb[i];
             pre.s_old[i] = pa[i] + pb[i];
         }
-        pre.alpha_it = BOX ? R(0) : alpha_it(kp);
+        pre.alpha_it = alpha_it(kp);
         pre.j_old = R(typename Store<R>::type(0.5)) * dot3(d, d) + penalty_x(pre.alpha_it);
-        pre.eps = eps_fn();
     }
 
     template <class Reload>
     __device__ __forceinline__ void finish(Reload& reload, const KP<R>& kp, const Pre& pre, Rec<R>& o) const {
         using T = typename Store<R>::type;
         const R half = R(T(0.5));
-        R pa[3], pb[3], d[3], mv[3];
+        R pa[3], pb[3], d[3];
         points(reload, pa, pb);
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            d[i] = pa[i] - pb[i];
-            mv[i] = (pa[i] + pb[i]) - pre.s_old[i];
-        }
+        for (int i = 0; i < 3; ++i) d[i] = pa[i] - pb[i];
         const R dd = dot3(d, d);
         const R jh = half * dd;
-        const R j_total = jh + penalty_x(pre.alpha_it);
         const R eps = pre.eps;
+        R dj, mv2;
+        if (BOX) {
+            // Last sweep's step dx = x - x_old: d moved by delta = sum dx_k E_k
+            // (E0, E1, E3, E4 as in init), so with g_k = d.E_k now,
+            //   J - J_old = sum dx_k g_k - |delta|^2 / 2,
+            // and S = pa + pb moved by dx0 E0 + dx1 E1 - dx2 E3 - dx3 E4;
+            // both squared lengths are quadratic forms in the Gram terms
+            // (qa, qb within A and B, xab between them).
+            const R e0 = x0 - pre.x_old[0], e1 = x1 - pre.x_old[1];
+            const R e2 = x2 - pre.x_old[2], e3 = x3 - pre.x_old[3];
+            const R lin = ((e0 * g0 + e1 * g1) + e2 * g3) + e3 * g4;
+            const R qa = e0 * (e0 * G00 + R(T(2)) * (e1 * G01)) + e1 * (e1 * G11);
+            const R qb = e2 * (e2 * G33 + R(T(2)) * (e3 * G34)) + e3 * (e3 * G44);
+            const R xab = e0 * (e2 * G03 + e3 * G04) + e1 * (e2 * G13 + e3 * G14);
+            const R qq = qa + qb;
+            dj = lin - half * (qq + R(T(2)) * xab);
+            mv2 = qq - R(T(2)) * xab;
+        } else {
+            R mv[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) mv[i] = (pa[i] + pb[i]) - pre.s_old[i];
+            dj = (jh + penalty_x(pre.alpha_it)) - pre.j_old;
+            mv2 = dot3(mv, mv);
+        }
         // move = |S - S_old| / 2 <= mf * eps, compared squared (no sqrt)
         const R mlim = kp.move_factor * eps;
-        const bool settled = (absv(j_total - pre.j_old) <= kp.c_factor * eps) &&
-                             (dot3(mv, mv) <= R(typename Store<R>::type(4)) * (mlim * mlim));
+        const bool settled = (absv(dj) <= kp.c_factor * eps) && (mv2 <= R(T(4)) * (mlim * mlim));
         const bool contact = settled && (jh <= (R(T(2)) * eps) * eps);
         o.kind = contact ? KIND_CONTACT : (settled ? KIND_NO_CONTACT : KIND_NOT_TERMINATED);
 #pragma unroll
