@@ -11,8 +11,10 @@ namespace tc {
 
 // Unrolling of the comparison kernel's crossing (X) and feature (F) test
 // loops: full unrolling makes every vertex index a compile-time constant.
+// Measured: X fully unrolled (3) is 3.5 % faster for the comparison kernel
+// and 1.2 % for the hybrid; unrolling F (3 or 9) is 4-7 % slower (spills).
 #ifndef TC_UNROLL_X
-#define TC_UNROLL_X 1
+#define TC_UNROLL_X 3
 #endif
 #ifndef TC_UNROLL_F
 #define TC_UNROLL_F 1
