@@ -381,6 +381,36 @@ struct Scratch {
     }
 };
 
+// Fast build: the weights (u, w) along (ab, ac) of a point known to lie in
+// the triangle (the midpoint of two crossing points, which lie in both
+// triangles up to rounding), from the 2x2 normal equations of the triangle's
+// frame -- for such a point the reference's closest point is the point
+// itself, its weights the same up to rounding (ill-conditioned triangles,
+// det < kappa * |ab|^2 |ac|^2, take the reference's region path).
+template <class R, class Tri>
+__device__ __forceinline__ void inside_point_params(const R* p, const Tri& tri, R& u, R& w) {
+    using T = typename Store<R>::type;
+    R a[3], ab[3], ac[3], ap[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        a[i] = tri[i];
+        ab[i] = tri[3 + i] - a[i];
+        ac[i] = tri[6 + i] - a[i];
+        ap[i] = p[i] - a[i];
+    }
+    const R uu = dot3(ab, ab), uv = dot3(ab, ac), vv = dot3(ac, ac);
+    const R det = uu * vv - uv * uv;
+    const R kappa = R(T(sizeof(T) == 8 ? 1e-6 : 1e-2));
+    if (!(det >= kappa * (uu * vv)) || det == R(0)) {
+        closest_point_params_t(p, tri, u, w);
+        return;
+    }
+    const R r = rcpv(det);
+    const R pu = dot3(ap, ab), pv = dot3(ap, ac);
+    u = (vv * pu - uv * pv) * r;
+    w = (uu * pv - uv * pu) * r;
+}
+
 template <class R, class Tri>
 __device__ __forceinline__ bool comparison_phase1(const Tri& A, const Tri& B, R eps, Scratch<R> cpts, Rec<R>& o) {
     using T = typename Store<R>::type;
@@ -459,8 +489,13 @@ __device__ __forceinline__ bool comparison_phase1(const Tri& A, const Tri& B, R 
     o.distance = R(0);
 #pragma unroll
     for (int i = 0; i < 3; ++i) { o.pa[i] = mid[i]; o.pb[i] = mid[i]; }
-    closest_point_params_t(mid, A, o.ba[0], o.ba[1]);
-    closest_point_params_t(mid, B, o.bb[0], o.bb[1]);
+    if constexpr (IsStrict<R>::value) {
+        closest_point_params_t(mid, A, o.ba[0], o.ba[1]);
+        closest_point_params_t(mid, B, o.bb[0], o.bb[1]);
+    } else {
+        inside_point_params(mid, A, o.ba[0], o.ba[1]);
+        inside_point_params(mid, B, o.bb[0], o.bb[1]);
+    }
     o.kind = (o.distance <= R(T(2)) * eps) ? KIND_CONTACT : KIND_NO_CONTACT;
     o.ids = ((uint32_t)bidx << 16) | ((uint32_t)FLAG_INTERSECT << 24);
     return true;
