@@ -46,7 +46,7 @@ def test_strict_oracle_against_itself_is_exact(oracle_lib, golden_inputs):
     assert rep["ok"] and rep["excused"] == 0 and rep["distance_max_rel"] == 0.0
 
 
-@pytest.mark.parametrize("col,delta", [("distance", 1e-7), ("point_a", 1e-6)])
+@pytest.mark.parametrize("col,delta", [("distance", 1e-7), ("point_a", 1e-6), ("bary_a", 1e-6), ("bary_b", 1e-6)])
 def test_checker_rejects_corruption(oracle_lib, golden_inputs, col, delta):
     A, B = golden_inputs["cfg0_A"][:512], golden_inputs["cfg0_B"][:512]
     got = _run(oracle_lib, "hybrid", A, B, PARAM_SETS["def"], np.float64)
