@@ -423,13 +423,22 @@ struct FlatSource {
         a.ids[4 * j] = (uint8_t)(ids & 0xFF);
         a.ids[4 * j + 1] = (uint8_t)((ids >> 8) & 0xFF);
     }
+    // row j keeps its (open: flags 0) iterative result; kind and flags say DEGENERATE
+    __device__ __forceinline__ void mark_degenerate(int64_t j) const {
+        if (a.kind) a.kind[j] = (int8_t)KIND_DEGENERATE;
+        if (a.ids) a.ids[4 * j + 3] = (uint8_t)FLAG_DEGENERATE;
+    }
 };
 
 // Run whole batches (QB pairs -- the CTA size --, or the remainder when
 // `final_`) from the queues until neither holds a full batch.  Block-uniform;
 // every batch runs on full warps.  `fallback_flag`: hybrid results carry
 // FLAG_FALLBACK.
-template <class R, class Src, int QB>
+// SCREEN: the batch's pairs are screened for degenerate triangles before
+// phase 1 (RK/kernels.py:596-600) -- on full warps of open pairs instead of
+// divergently in the producing tile; a degenerate pair keeps its iterative
+// result and is marked DEGENERATE (src.mark_degenerate).
+template <bool SCREEN = false, class R, class Src, int QB>
 __device__ __forceinline__ void drain(const Src& src, Queues<QB>& Q, Tally& tl, bool final_, uint32_t fallback_flag) {
     const bool want_ids = src.want_ids();
     while (true) {
@@ -456,7 +465,16 @@ __device__ __forceinline__ void drain(const Src& src, Queues<QB>& Q, Tally& tl, 
             R eps;
             src.stage(j, A, B, eps);
             Rec<R> r;
-            if (which == 1) {
+            bool screened = false;
+            if constexpr (SCREEN) {
+                if (which == 1 && (degenerate_tri_t<R>(A) || degenerate_tri_t<R>(B))) {
+                    src.mark_degenerate(j);
+                    tl.degenerate++;
+                    screened = true;
+                }
+            }
+            if (screened) {
+            } else if (which == 1) {
                 tl.comparison++;
                 if (comparison_phase1(A, B, eps, thread_scratch<R, QB>(), r)) {
                     r.ids |= fallback_flag << 24;
@@ -515,9 +533,9 @@ __global__ void __launch_bounds__(BS_CMP, TC_MINB(BS_CMP, 2)) comparison_kernel(
         }
         push(Q.q2, &Q.n2, need2, e2);
         __syncthreads();
-        drain<R>(FlatSource<SOA, R, T, BS_CMP>{a, thread_slot<T>(SCR * BS_CMP)}, Q, tl, false, 0u);
+        drain<false, R>(FlatSource<SOA, R, T, BS_CMP>{a, thread_slot<T>(SCR * BS_CMP)}, Q, tl, false, 0u);
     }
-    drain<R>(FlatSource<SOA, R, T, BS_CMP>{a, thread_slot<T>(SCR * BS_CMP)}, Q, tl, true, 0u);
+    drain<false, R>(FlatSource<SOA, R, T, BS_CMP>{a, thread_slot<T>(SCR * BS_CMP)}, Q, tl, true, 0u);
     // comparison_batch alone counts as comparison work but not as a fallback
     tl.flush<false>(a.stats);
 }
@@ -594,16 +612,9 @@ __global__ void __launch_bounds__(BS_HYB, TC_MINB(BS_HYB, TC_HYBRID_MINB)) hybri
             Rec<R> r;
             run_iterative<BS_HYB>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
             tl.iterative++;
-            if (r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i])) {
-                const SmemTri<R> SA{slot, BS_HYB}, SB{slot + 9 * BS_HYB, BS_HYB};
-                if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {
-                    r.kind = KIND_DEGENERATE;
-                    r.ids |= (uint32_t)FLAG_DEGENERATE << 24;
-                    tl.degenerate++;
-                } else {
-                    enq = true;
-                }
-            }
+            // open pairs are queued; the phase-1 batches screen them for
+            // degenerate triangles (drain<SCREEN>)
+            enq = r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i]);
             // every lane stores its tile result now (open pairs a placeholder
             // the fallback overwrites), so output sectors are written whole
             store_rec<SOA>(a, i, r);
@@ -611,9 +622,9 @@ __global__ void __launch_bounds__(BS_HYB, TC_MINB(BS_HYB, TC_HYBRID_MINB)) hybri
         }
         push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
-        drain<R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+        drain<true, R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
-    drain<R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    drain<true, R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     tl.flush<true>(a.stats);
 }
 
@@ -797,9 +808,9 @@ __global__ void __launch_bounds__(BS_BLK, TC_MINB(BS_BLK, TC_HYBRID_MINB)) block
             }
             push(Q.q1, &Q.n1, enq, p);
             __syncthreads();
-            drain<R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+            drain<false, R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
         }
-        drain<R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+        drain<false, R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     }
     tl.flush<true>(a.stats);
 }
@@ -945,9 +956,9 @@ __global__ void __launch_bounds__(BS_FRONT, TC_MINB(BS_FRONT, TC_HYBRID_MINB)) f
         }
         push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
-        drain<R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+        drain<false, R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
-    drain<R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    drain<false, R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     __syncthreads();
     if (threadIdx.x <= (unsigned)a.max_height && threadIdx.x < 32 && hist[threadIdx.x])
         atomicAdd(a.checks + threadIdx.x, hist[threadIdx.x]);
