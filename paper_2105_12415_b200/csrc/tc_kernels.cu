@@ -722,6 +722,8 @@ struct BlockSource {
             if (a.c_pb) a.c_pb[3 * slot + c] = val(r.pb[c]);
         }
     }
+    // degenerate pairs are counted, never emitted as contacts
+    __device__ __forceinline__ void mark_degenerate(int64_t) const {}
     __device__ __forceinline__ void store_ids01(int64_t, uint32_t) const {}
 };
 
@@ -793,14 +795,7 @@ __global__ void __launch_bounds__(BS_BLK, TC_MINB(BS_BLK, TC_HYBRID_MINB)) block
                 Rec<R> r;
                 run_iterative(SA, SB, A, B, [&] { return eps; }, kp, r);
                 tl.iterative++;
-                if (r.kind == KIND_NOT_TERMINATED) {
-                    if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {
-                        r.kind = KIND_DEGENERATE;
-                        tl.degenerate++;
-                    } else {
-                        enq = true;
-                    }
-                }
+                enq = r.kind == KIND_NOT_TERMINATED;  // screened for degeneracy in the batches
                 if (!enq) {
                     src.store(p, r);
                     tl.result(r);
@@ -808,9 +803,9 @@ __global__ void __launch_bounds__(BS_BLK, TC_MINB(BS_BLK, TC_HYBRID_MINB)) block
             }
             push(Q.q1, &Q.n1, enq, p);
             __syncthreads();
-            drain<false, R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+            drain<true, R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
         }
-        drain<false, R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+        drain<true, R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     }
     tl.flush<true>(a.stats);
 }
@@ -908,6 +903,7 @@ struct FrontierSource {
             a.c_pb[3 * slot + c] = val(r.pb[c]);
         }
     }
+    __device__ __forceinline__ void mark_degenerate(int64_t j) const { a.kind[j] = (int8_t)KIND_DEGENERATE; }
     __device__ __forceinline__ void store_ids01(int64_t, uint32_t) const {}
 };
 
@@ -940,15 +936,7 @@ __global__ void __launch_bounds__(BS_FRONT, TC_MINB(BS_FRONT, TC_HYBRID_MINB)) f
             run_iterative<BS_FRONT>(slot, A, B,
                           [&] { return R(T(0.5)) * (R(a.node_eps[ia]) + R(a.node_eps[ib])); }, kp, r);
             tl.iterative++;
-            if (r.kind == KIND_NOT_TERMINATED && both_fine) {
-                const SmemTri<R> SA{slot, BS_FRONT}, SB{slot + 9 * BS_FRONT, BS_FRONT};
-                if (degenerate_tri_t<R>(SA) || degenerate_tri_t<R>(SB)) {
-                    r.kind = KIND_DEGENERATE;
-                    tl.degenerate++;
-                } else {
-                    enq = true;
-                }
-            }
+            enq = r.kind == KIND_NOT_TERMINATED && both_fine;  // screened for degeneracy in the batches
             if (!enq) {
                 src.store(i, r);
                 tl.result(r);
@@ -956,9 +944,9 @@ __global__ void __launch_bounds__(BS_FRONT, TC_MINB(BS_FRONT, TC_HYBRID_MINB)) f
         }
         push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
-        drain<false, R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
+        drain<true, R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
-    drain<false, R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
+    drain<true, R>(src, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     __syncthreads();
     if (threadIdx.x <= (unsigned)a.max_height && threadIdx.x < 32 && hist[threadIdx.x])
         atomicAdd(a.checks + threadIdx.x, hist[threadIdx.x]);
