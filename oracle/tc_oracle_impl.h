@@ -56,6 +56,7 @@ static __thread double FN(tl_pt_d_), FN(tl_pt_v_), FN(tl_seg_), FN(tl_cx_plane_)
 
 static inline double FN(fabsd_)(double x) { return x < 0 ? -x : x; }
 static inline double FN(mind_)(double a, double b) { return a < b ? a : b; }
+static inline double FN(max_d_)(double a, double b) { return a > b ? a : b; }
 
 /* RK/geometry.py:68-75 degenerate_mask (rel_tol = 1e-12). */
 static int FN(degenerate_one_)(const REAL* t) {
@@ -171,7 +172,9 @@ static int FN(segment_segment_)(const REAL* p1, const REAL* q1, const REAL* p2, 
     REAL denom = t1 - t2;
     int code = 0;
     REAL s;
-    double sm = 1e300;
+    /* the solve / parallel decision: denom = a e sin^2(angle) is rounding
+     * noise for nearly parallel segments, so its margin is |denom| / (a e) */
+    double sm = FN(fabsd_)((double)denom) / FN(max_d_)((double)a * (double)e, 1e-300);
     if (denom > TC_TINY_) {
         code |= 1;
         t1 = b * f;
@@ -711,7 +714,8 @@ int FN(tco_hybrid_)(const REAL* A, const REAL* B, int64_t n, const REAL* eps,
  * feature distance, [1] distance - 2 eps, [2] min endpoint-to-plane distance
  * of the six crossing tests, [3] min barycentric inside margin of the tests
  * whose endpoints straddle the plane, [4] |dJ| - c eps, [5] move - mf eps,
- * [6] J_hat - 2 eps^2, [7] normalised region / segment-branch margin of the
+ * [6] J_hat - 2 eps^2, [7] normalised region / segment-branch margin (incl. the
+ * solve-or-parallel decision, |denom| / (a e)) of the
  * winning feature, [8] the feature distance before the crossing override
  * (the answer had no crossing been found), [9] max conditioning
  * (uu + vv)^2 / |det| of the six barycentric solves.  Test-side tie
