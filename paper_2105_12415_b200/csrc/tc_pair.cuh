@@ -620,26 +620,11 @@ __device__ __forceinline__ void comparison_phase2_impl(const Tri& A, const Tri& 
     o.ids |= 255u << 16;
 }
 
-// Phase 2 entry: the 15 tests re-read the pair's vertices many times, so
-// with TC_P2_REGS the pair is first copied from its shared-memory slot into
-// registers (phase 2 no longer shares the register file with the crossing
-// list or the iterative state).
-#ifndef TC_P2_REGS
-#define TC_P2_REGS 0  // measured slower (spills at the 128-register cap): off
-#endif
+// Phase 2 entry (the pair stays in its shared-memory slot: copying it into
+// registers first measured slower -- spills at the 128-register cap).
 template <class R, class Tri>
 __device__ __forceinline__ void comparison_phase2(const Tri& A, const Tri& B, R eps, bool ids_only, Rec<R>& o) {
-#if TC_P2_REGS
-    R a[9], b[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-        a[k] = A[k];
-        b[k] = B[k];
-    }
-    comparison_phase2_impl(RegTri<R>{a}, RegTri<R>{b}, eps, ids_only, o);
-#else
     comparison_phase2_impl(A, B, eps, ids_only, o);
-#endif
 }
 
 // RK/kernels.py:417-431 _penalty_value, summed left to right.
@@ -671,9 +656,10 @@ __device__ __forceinline__ void contact_mid(const R* A0, const R* x, const R* e1
 // cycles of latency on B200 (tools/latency_probe.cu: DFMA + one min = 24
 // cycles, DFMA + a two-sided fmax/fmin clip = 58), and the iterative kernel
 // is one long chain of clips.  The lower clip at 0 is a sign-bit test on the
-// integer pipe.  TC_INT_CLIP=1 also does the upper compare on 64-bit integer
-// patterns (for non-negative IEEE values the patterns order like the values);
-// measured slower (9.2 vs 9.9 G pairs/s iterative), so it is off.
+// integer pipe.  Doing the upper compare on 64-bit integer patterns too (for
+// non-negative IEEE values the patterns order like the values) measured
+// slower: more instructions (two ISETP + selects) and a longer chain, and
+// the sweep is issue-bound.  The fp32 clips are integer clips.
 // NaN inputs are not supported.
 //
 // clip0_hi(x, hi) == np.clip(x, 0, hi) bit for bit for hi >= +0 (x <= 0,
@@ -687,23 +673,13 @@ __device__ __forceinline__ float negv(float x) { return __int_as_float(__float_a
 template <typename T>
 __device__ __forceinline__ Strict<T> negv(Strict<T> x) { return -x; }
 
-#ifndef TC_INT_CLIP
-#define TC_INT_CLIP 0
-#endif
 __device__ __forceinline__ double clip0_hi(double x, double hi) {
-#if TC_INT_CLIP
-    long long xb = __double_as_longlong(x);
-    const long long hb = __double_as_longlong(hi);
-    xb = (xb < 0) ? 0 : xb;
-    return __longlong_as_double(xb < hb ? xb : hb);
-#else
     // both tests read the unclipped x, so they issue in parallel (one compare
     // latency on the chain instead of two); equal to min(max(x, 0), hi) for
     // hi >= +0, including signed zeros
     const bool neg = __double2hiint(x) < 0;
     const double r = (x < hi) ? x : hi;
     return neg ? 0.0 : r;
-#endif
 }
 __device__ __forceinline__ float clip0_hi(float x, float hi) {
     int xb = __float_as_int(x);
@@ -717,17 +693,10 @@ __device__ __forceinline__ Strict<T> clip0_hi(Strict<T> x, Strict<T> hi) { retur
 // clip(t, -xb, xa) for xa, xb >= 0 (the fast build's box mode): clip the
 // magnitude against the bound on t's side, keep t's sign.
 __device__ __forceinline__ double clip_sym(double t, double xb, double xa) {
-#if !TC_INT_CLIP
     // independent compares of the unclipped t against both bounds
     const double lo = negv(xb);
     const bool below = !(t > lo), above = !(t < xa);
     return below ? lo : (above ? xa : t);
-#endif
-    const long long tb = __double_as_longlong(t);
-    const long long mag = tb & 0x7FFFFFFFFFFFFFFFLL;
-    const long long lim = (tb < 0) ? __double_as_longlong(xb) : __double_as_longlong(xa);
-    const long long r = mag < lim ? mag : lim;
-    return __longlong_as_double(r | (tb & (long long)0x8000000000000000ULL));
 }
 __device__ __forceinline__ float clip_sym(float t, float xb, float xa) {
     const int tb = __float_as_int(t);
