@@ -70,7 +70,8 @@ constexpr int BS_ITER = TC_BS_ITER, BS_HYB = TC_BS_HYB, BS_CMP = TC_BS_CMP, BS_B
 #define TC_PREFETCH 1
 #endif
 // dynamic shared memory of the comparison phases, per thread (stride BLOCK):
-// [crossing points: SCR values (at most 4 points, see comparison_phase1)]
+// [crossing points: SCR values (at most 4 points, see comparison_phase1);
+//  in phase 2 the hoisted edge lengths and reciprocals]
 // [pair slot: SLOT values]
 constexpr int SCR = 12;
 constexpr int SLOT = 18;
@@ -488,7 +489,7 @@ __device__ __forceinline__ void drain(const Src& src, Queues<QB>& Q, Tally& tl, 
                 }
             } else {
                 const bool ids_only = (e & IDS_ONLY) != 0;
-                comparison_phase2(A, B, eps, ids_only, r);
+                comparison_phase2(A, B, eps, ids_only, r, thread_scratch<R, QB>());
                 if (ids_only) {
                     src.store_ids01(j, r.ids);
                 } else {
