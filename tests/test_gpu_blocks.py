@@ -125,3 +125,35 @@ def test_blocks_fused_rigid_motion(oracle_lib, strict):
         p = oracle_lib.make_params(**pk)
         ref, _, _ = oracle_lib.hybrid(A, B, p, p.epsilon, threads=oracle_lib.default_threads())
         assert a["n_contacts"] == int((ref["kind"] == 1).sum())
+
+
+@pytest.mark.parametrize("strict", [True, False])
+def test_blocks_degenerate_screen(oracle_lib, scene, strict):
+    """Degenerate triangles among the open (fallback) pairs of a block are
+    counted, never compared or emitted (RK/kernels.py:596-600); the screen
+    runs in the fallback batches.  Strict: counts equal the oracle's."""
+    meshes, blocks, gaps = scene
+    which = [int(np.argmin(gaps))]
+    a_mesh = int(blocks[which[0], 0])
+    bad = meshes.copy()
+    tri = bad[a_mesh]
+    sel = np.arange(0, tri.shape[0], 5)
+    tri[sel, 2] = tri[sel, 0] + 0.5 * (tri[sel, 1] - tri[sel, 0])   # collinear: zero area
+    pkw = dict(n_iterative=4, epsilon=5e-2)   # halo wide enough for open pairs
+    st = D.new_stats()
+    out = PT.blocks_hybrid(torch.from_numpy(bad).cuda(), torch.from_numpy(blocks[which]).cuda(),
+                           D.Params(**pkw), strict=strict, stats=st)
+    torch.cuda.synchronize()
+    got = PT.sort_contacts(out)
+    s = D.read_stats(st)
+    A, B = PT.block_pairs(bad, blocks, which)
+    p = oracle_lib.make_params(**pkw)
+    ref, counts, rc = oracle_lib.hybrid(A, B, p, p.epsilon, threads=oracle_lib.default_threads())
+    assert counts[3] > 0 and rc != 0          # the oracle marks them (and would raise)
+    assert s["degenerate"] > 0
+    if strict:
+        T = bad.shape[1]
+        idx, dist, _, _ = _contacts_from_flat(ref["kind"], ref["distance"], ref["point_a"], ref["point_b"],
+                                              range(len(which)), T)
+        assert [s["iterative"], s["comparison"], s["fallback"], s["degenerate"]] == list(counts[:4])
+        assert np.array_equal(got["idx"], idx) and np.array_equal(got["distance"], dist)

@@ -271,3 +271,33 @@ def test_start_coord_general(oracle_lib, real, start):
         if variant == "hybrid":
             for k in COLS:
                 assert np.array_equal(strict[k].cpu().numpy(), ref[k]), k
+
+
+@pytest.mark.parametrize("soa", [False, True])
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_degenerate_screen_random(oracle_lib, real, soa):
+    """Degenerate triangles injected into random pairs, with a per-pair
+    fallback mask and per-pair halos: the fallback batches screen them
+    (kind 3, DEGENERATE flag, counted, not compared) exactly like the
+    oracle's hybrid (strict: bitwise incl. ids and counters)."""
+    dt = DTYPES[real]
+    A, B = W.random_pairs(3 * 4096 + 5, seed=21, sep=(-0.1, 0.5))
+    rng = np.random.default_rng(9)
+    for T in (A, B):
+        sel = rng.random(len(T)) < 0.05
+        T[sel, 2] = T[sel, 0] + 0.25 * (T[sel, 1] - T[sel, 0])
+    A = A.astype(dt)
+    B = B.astype(dt)
+    eps = rng.uniform(1e-7, 1e-5, len(A)).astype(dt)
+    allow = (rng.random(len(A)) < 0.9).astype(np.uint8)
+    pk = PARAM_SETS["bl"]
+    got, st = run_dev("hybrid", A, B, real, "bl", True, soa=soa, eps=eps, allow=allow)
+    ref, counts, rc = oracle_lib.hybrid(A, B, oracle_lib.make_params(**pk), eps, allow_fallback=allow, dtype=dt)
+    assert rc != 0 and counts[3] > 0
+    for k in COLS:
+        assert np.array_equal(got[k], ref[k]), k
+    assert np.array_equal(got["ids"], ref["ids"])
+    assert [st["iterative"], st["comparison"], st["fallback"], st["degenerate"]] == list(counts[:4])
+    fast, fst = run_dev("hybrid", A, B, real, "bl", False, soa=soa, eps=eps, allow=allow)
+    assert fst["degenerate"] > 0
+    assert np.all((fast["ids"][fast["kind"] == 3, 3] & 8) > 0)
