@@ -38,3 +38,25 @@ for name, (A, B) in sets.items():
         rep["check_s"] = round(time.time() - t0, 1)
         rep["stats"] = D.read_stats(st)
         print(f"{name} {np.dtype(dt).name}: {rep}", flush=True)
+
+# Strict build: bit-identical to the oracle (= the reference) on every pair of
+# the full cfg1 batch (2^24) and the full cfg3 set, both precisions.
+full = {"cfg1 (2^24, the bench batch)": W.random_pairs_mp(1 << 24, seed=0, sep=(-0.1, 0.5)),
+        "cfg3 (4 x 2^20 adversarial)": sets["cfg3 (4 x 2^20 adversarial)"]}
+for name, (A, B) in full.items():
+    for dt, tdt in ((np.float64, torch.float64), (np.float32, torch.float32)):
+        a = np.ascontiguousarray(A, dt)
+        b = np.ascontiguousarray(B, dt)
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        st = D.new_stats()
+        out = D.run("hybrid", ta, tb, D.Params(**PK), strict=True, ids=True, stats=st)
+        torch.cuda.synchronize()
+        got = {k: v.cpu().numpy() for k, v in out.items()}
+        del ta, tb, out
+        ref, counts, rc = oracle.hybrid(a, b, oracle.make_params(**PK), PK["epsilon"], dtype=dt,
+                                        threads=oracle.default_threads())
+        diff = {k: int((got[k] != ref[k]).reshape(len(a), -1).any(axis=1).sum()) for k in ref}
+        s = D.read_stats(st)
+        same_counts = [s["iterative"], s["comparison"], s["fallback"], s["degenerate"]] == list(counts[:4])
+        print(f"STRICT {name} {np.dtype(dt).name}: n={len(a)} rows differing per column {diff} "
+              f"counters equal {same_counts} rc {rc}", flush=True)
