@@ -9,9 +9,9 @@
 //   hybrid_kernel      RK/kernels.py:568-605 -- iterative for a tile of one
 //       pair per thread, NOT_TERMINATED lanes (with allow_fb) are appended to
 //       a shared-memory queue by warp ballot; whenever the queue holds a full
-//       CTA of pairs, all threads run the comparison phases on it, so the
-//       divergent fallback executes on full warps.  The fallback never
-//       leaves the kernel.
+//       CTA of pairs, all threads screen them for degenerate triangles and
+//       run the comparison phases on them, so the divergent fallback executes
+//       on full warps.  The fallback never leaves the kernel.
 //   blocks_hybrid_kernel  all-pairs particle blocks (RK/stepping.py:285-308,
 //       RK/contact.py:97-140): both meshes staged in shared memory, optional
 //       fused rigid motions (RK/geometry.py:162-176)
@@ -585,10 +585,11 @@ __global__ void __launch_bounds__(BS_ITER, TC_MINB(BS_ITER, TC_ITER_MINB)) itera
 // measured slower than two 256-thread CTAs.)
 
 // RK/kernels.py:568-605.  Per tile of BLOCK pairs: the iterative kernel on
-// every lane; open (NOT_TERMINATED, fallback allowed, non-degenerate) pairs
-// are appended to q1; full batches of q1 run phase 1 of the comparison
-// kernel and non-intersecting ones move on to q2 for phase 2 -- so both
-// fallback phases execute on full warps, inside this kernel.  (Running
+// every lane; open (NOT_TERMINATED, fallback allowed) pairs are appended to
+// q1; full batches of q1 are screened for degenerate triangles and run phase
+// 1 of the comparison kernel, and non-intersecting ones move on to q2 for
+// phase 2 -- so the screen and both fallback phases execute on full warps,
+// inside this kernel.  (Running
 // phase 1 in-tile on the compacted open lanes, straight from the owners'
 // shared-memory slots, saves the re-read of queued pairs but idles half the
 // warps: measured 8% slower on cfg1.)
