@@ -512,7 +512,9 @@ def configs_table(D, torch, dev):
     res["cfg3_fast"] = c3
     res["multiscale"] = multiscale_table(D, torch, dev)
     res["note"] = ("oracle agreement of cfg2/cfg3: tests/test_gpu_blocks.py, tests/test_gpu_cfg3.py "
-                   "(strict bitwise, fast within tolerance with the tie classifier)")
+                   "(strict bitwise, fast within tolerance with the tie classifier); at full size "
+                   "profiles/r01_parity_full.txt (all 4 x 2^20 cfg3 pairs: strict bitwise, fast within "
+                   "tolerance, fp64 and fp32) and profiles/r01_parity_cfg2.txt (all 576.7M cfg2 pairs)")
     return res
 
 
