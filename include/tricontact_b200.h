@@ -254,6 +254,14 @@ int64_t tc_fma_probe(int fp64, int64_t blocks, int iters, void* sink, void* stre
 /* Number of kernel launches this library has enqueued since load. */
 int64_t tc_launch_count(void);
 
+/* reduce a device tc_stats over the ranks of an NCCL
+ * communicator -- one ncclGroupStart/End with ncclAllReduce(int64[6], sum)
+ * and ncclAllReduce(double[1], min), enqueued on `stream` (no host sync).
+ * nccl_comm: an ncclComm_t the caller created.  libnccl.so.2 is dlopen'ed on
+ * first use (TC_ENODEVICE if absent); the other entry points never need it.
+ * Python hosts may use torch.distributed instead (paper_2105_12415_b200/shard.py). */
+int tc_allreduce_stats(tc_stats* stats, void* nccl_comm, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -57,6 +57,7 @@ SIGNATURES = {
     "tc_abi_version": (_INT, []),
     "tc_last_error": (ctypes.c_char_p, []),
     "tc_launch_count": (_I64, []),
+    "tc_allreduce_stats": (_INT, [_P, _P, _P]),
     "tc_stats_reset": (_INT, [_P, _P]),
     "tc_fma_probe": (_I64, [_INT, _I64, _INT, _P, _P]),
     "tc_closest_point_triangle_f64": (_INT, [_P, _P, _I64, _P, _P, _P]),

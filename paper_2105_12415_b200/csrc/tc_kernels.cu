@@ -30,6 +30,8 @@
 #include <cub/device/device_scan.cuh>
 #include <vector>
 #include <mutex>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is dlopen'ed on first use (tc_allreduce_stats)
 
 #include "tc_pair.cuh"
 #include "../../include/tricontact_b200.h"
@@ -1581,6 +1583,67 @@ void tc_params_default(tc_params* p) {
 int tc_abi_version(void) { return TC_ABI_VERSION; }
 const char* tc_last_error(void) { return tc::g_err; }
 int64_t tc_launch_count(void) { return tc::g_launches.load(); }
+
+}  // extern "C"
+
+namespace tc {
+// NCCL entry points, resolved from libnccl.so.2 on first use so the library
+// loads (and every other entry point works) without NCCL present.  A process
+// that already loaded an NCCL (e.g. torch's) gets that copy: same soname.
+struct NcclApi {
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+static const NcclApi* nccl_api() {
+    static NcclApi api;
+    static bool ok = false;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+        api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+        api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+        ok = api.group_start && api.group_end && api.all_reduce && api.error_string;
+    });
+    return ok ? &api : nullptr;
+}
+}  // namespace tc
+
+extern "C" {
+
+int tc_allreduce_stats(tc_stats* stats, void* nccl_comm, void* stream) {
+    if (!stats || !nccl_comm) {
+        snprintf(tc::g_err, sizeof(tc::g_err), "tc_allreduce_stats: NULL stats or communicator");
+        return TC_EINVAL;
+    }
+    const tc::NcclApi* api = tc::nccl_api();
+    if (!api) {
+        snprintf(tc::g_err, sizeof(tc::g_err), "tc_allreduce_stats: libnccl.so.2 not found");
+        return TC_ENODEVICE;
+    }
+    auto comm = reinterpret_cast<ncclComm_t>(nccl_comm);
+    auto s = reinterpret_cast<cudaStream_t>(stream);
+    // one group: SUM of the six int64 tallies, MIN of the fp64 minimum distance
+    ncclResult_t r = api->group_start();
+    if (r == ncclSuccess) {
+        const ncclResult_t r1 = api->all_reduce(stats, stats, 6, ncclInt64, ncclSum, comm, s);
+        const ncclResult_t r2 =
+            api->all_reduce(&stats->min_distance, &stats->min_distance, 1, ncclFloat64, ncclMin, comm, s);
+        r = api->group_end();
+        if (r1 != ncclSuccess) r = r1;
+        else if (r2 != ncclSuccess) r = r2;
+    }
+    if (r != ncclSuccess) {
+        snprintf(tc::g_err, sizeof(tc::g_err), "tc_allreduce_stats: %s", api->error_string(r));
+        return TC_ECUDA;
+    }
+    return TC_OK;
+}
 
 int64_t tc_fma_probe(int fp64, int64_t blocks, int iters, void* sink, void* stream) {
     if (blocks < 1 || iters < 1 || !sink) return -1;

@@ -79,3 +79,38 @@ def test_sharded_tallies_equal_whole(oracle_lib, golden_inputs):
                 assert np.array_equal(o[k], whole[k][lo:lo + c])
         assert np.array_equal(tot, counts)
         assert min(mins) == whole["distance"].min()
+
+
+@pytest.mark.gpu
+def test_c_abi_allreduce_stats_one_rank():
+    """tc_allreduce_stats (the C-ABI reduction for non-torch hosts) on a
+    1-rank NCCL communicator: the grouped SUM / MIN leaves the record as is;
+    a NULL communicator is TC_EINVAL."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import ctypes
+    from paper_2105_12415_b200 import _abi, device as D
+    nccl = ctypes.CDLL("libnccl.so.2", mode=ctypes.RTLD_GLOBAL)
+
+    class UniqueId(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_char * 128)]
+
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm = ctypes.c_void_p()
+    torch.cuda.set_device(0)
+    assert nccl.ncclCommInitRank(ctypes.byref(comm), 1, uid, 0) == 0
+    try:
+        st = D.new_stats()
+        st[:6] = torch.tensor([5, 4, 4, 1, 3, 2], dtype=torch.int64)
+        st[6:].view(torch.float64)[0] = 0.25
+        before = st.clone()
+        lib = _abi.load()
+        s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        assert lib.tc_allreduce_stats(ctypes.c_void_p(st.data_ptr()), comm, s) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(st, before)
+        assert lib.tc_allreduce_stats(ctypes.c_void_p(st.data_ptr()), None, s) == 1   # TC_EINVAL
+    finally:
+        nccl.ncclCommDestroy(comm)
