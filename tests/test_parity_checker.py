@@ -60,3 +60,19 @@ def test_checker_rejects_flipped_kind(oracle_lib, golden_inputs):
     far = np.nonzero(got["distance"] > 0.1)[0][:3]
     got["kind"][far] = 1
     assert not parity.compare_fast(oracle_lib, "comparison", A, B, PARAM_SETS["def"], got, np.float64)["ok"]
+
+
+def test_bary_err_is_in_point_units():
+    """Weights along a sliver's two nearly parallel long edges are
+    ill-conditioned; the checker judges them by the point they name
+    (tests/parity.py bary_err): a weight change of 1e-4 that moves the point
+    by 1e-10 passes at tau = 1e-9, one that moves it by 1e-4 does not."""
+    T = np.array([[[0.0, 0, 0], [1.0, 0, 0], [0.5, 1e-6, 0]]])   # ab ~ 2 ac: height 5e-7
+    ref = {"bary_a": np.array([[0.25, 0.5]]), "bary_b": np.array([[0.25, 0.5]])}
+    L = parity.longest_edge(T, T)
+    d = 1e-4
+    along = {"bary_a": np.array([[0.25 - 0.5 * d, 0.5 + d]]), "bary_b": ref["bary_b"]}   # moves the point by 1e-10
+    across = {"bary_a": np.array([[0.25 + d, 0.5]]), "bary_b": ref["bary_b"]}           # moves it by 1e-4
+    assert parity.bary_err(T, T, along, ref, L)[0] < 1e-9
+    assert parity.bary_err(T, T, across, ref, L)[0] > 1e-5
+    assert np.allclose(parity.bary_point(T, ref["bary_a"]), [[0.5, 5e-7, 0.0]])
