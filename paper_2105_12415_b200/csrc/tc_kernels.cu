@@ -31,7 +31,15 @@
 #include <vector>
 #include <mutex>
 #include <dlfcn.h>
+#if __has_include(<nccl.h>)
 #include <nccl.h>  // types only: libnccl.so.2 is dlopen'ed on first use (tc_allreduce_stats)
+#else
+// the few NCCL types tc_allreduce_stats uses (ABI-stable values of nccl.h)
+typedef struct ncclComm* ncclComm_t;
+typedef enum { ncclSuccess = 0 } ncclResult_t;
+typedef enum { ncclSum = 0, ncclMin = 3 } ncclRedOp_t;
+typedef enum { ncclInt64 = 4, ncclFloat64 = 8 } ncclDataType_t;
+#endif
 
 #include "tc_pair.cuh"
 #include "../../include/tricontact_b200.h"
