@@ -303,26 +303,30 @@ def test_degenerate_screen_random(oracle_lib, real, soa):
     assert np.all((fast["ids"][fast["kind"] == 3, 3] & 8) > 0)
 
 
+@pytest.mark.parametrize("real", list(DTYPES))
 @pytest.mark.parametrize("strict", [True, False])
-def test_host_pipeline_equals_device(strict):
+def test_host_pipeline_equals_device(strict, real):
     """tc_run_host_f64 (pinned staging, 1M-pair chunks over 3 streams: the
     drop-in's path) gives the device entry point's results bit for bit on a
     batch of several chunks with a ragged tail, and the same counters."""
     import ctypes
     from paper_2105_12415_b200 import _abi
     n = (5 << 19) + 123   # 2.5 chunks of 2^20
+    dt = DTYPES[real]
     A, B = W.random_pairs(n, seed=4, sep=(-0.1, 0.5))
+    A, B = A.astype(dt), B.astype(dt)
     p = D.Params(**PARAM_SETS["bl"])
     st = D.new_stats()
     dev = D.run("hybrid", torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), p, strict=strict, stats=st)
     torch.cuda.synchronize()
     ds = D.read_stats(st)
-    out = {"distance": np.empty(n), "point_a": np.empty((n, 3)), "point_b": np.empty((n, 3)),
-           "bary_a": np.empty((n, 2)), "bary_b": np.empty((n, 2)), "kind": np.empty(n, np.int8)}
+    out = {"distance": np.empty(n, dt), "point_a": np.empty((n, 3), dt), "point_b": np.empty((n, 3), dt),
+           "bary_a": np.empty((n, 2), dt), "bary_b": np.empty((n, 2), dt), "kind": np.empty(n, np.int8)}
     ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
     hs = _abi.TcStats(0, 0, 0, 0, 0, 0, float("inf"))
     prm = _abi.params_struct(p, _abi.TC_STRICT if strict else 0)
-    rc = _abi.load().tc_run_host_f64(2, ptr(A), ptr(B), n, None, None, ctypes.byref(prm),
+    host = getattr(_abi.load(), "tc_run_host_f64" if real == "float64" else "tc_run_host_f32")
+    rc = host(2, ptr(A), ptr(B), n, None, None, ctypes.byref(prm),
                                      *(ptr(out[k]) for k in ("distance", "point_a", "point_b", "bary_a", "bary_b")),
                                      ptr(out["kind"]), None, ctypes.byref(hs))
     assert rc == 0
