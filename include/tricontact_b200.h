@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define TC_ABI_VERSION 1
+#define TC_ABI_VERSION 2
 
 /* return codes */
 #define TC_OK 0
@@ -145,9 +145,12 @@ int tc_point_triangle_distance_f32(const float* points, const float* tris, int64
                                    const int32_t* tri_index, int64_t n, float* distance,
                                    float* closest, void* stream);
 
-/* RK/geometry.py:68 degenerate_mask (rel_tol 1e-12): tris (n,3,3) -> mask (n,). */
-int tc_degenerate_mask_f64(const double* tris, int64_t n, uint8_t* mask, void* stream);
-int tc_degenerate_mask_f32(const float* tris, int64_t n, uint8_t* mask, void* stream);
+/* RK/geometry.py:68 degenerate_mask(tris, rel_tol): tris (n,3,3) -> mask (n,);
+ * flags sq_area < rel_tol * longest_sq^2 (rel_tol rounded to the dtype, like
+ * the reference's Python float times a REAL array; the reference default is
+ * 1e-12, which the hybrid's fallback screen always uses). */
+int tc_degenerate_mask_f64(const double* tris, int64_t n, double rel_tol, uint8_t* mask, void* stream);
+int tc_degenerate_mask_f32(const float* tris, int64_t n, double rel_tol, uint8_t* mask, void* stream);
 
 /* ---- all-pairs particle blocks (BASELINE.json config 2) -------------------
  * meshes: [n_meshes][tris_per_mesh][9] world-space triangles (device), or
@@ -242,8 +245,8 @@ int tc_closest_point_triangle_host_f64(const double* points, const double* tris,
                                        double* closest, double* bary);
 int tc_closest_point_triangle_host_f32(const float* points, const float* tris, int64_t n,
                                        float* closest, float* bary);
-int tc_degenerate_mask_host_f64(const double* tris, int64_t n, uint8_t* mask);
-int tc_degenerate_mask_host_f32(const float* tris, int64_t n, uint8_t* mask);
+int tc_degenerate_mask_host_f64(const double* tris, int64_t n, double rel_tol, uint8_t* mask);
+int tc_degenerate_mask_host_f32(const float* tris, int64_t n, double rel_tol, uint8_t* mask);
 
 /* FMA-pipe throughput probe (fp64 != 0: DFMA, else FFMA): enqueues one launch
  * of `blocks` CTAs and returns its flop count (or -1); time it with events

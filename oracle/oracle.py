@@ -77,7 +77,7 @@ def lib():
             getattr(_lib, f"tco_iterative_{sfx}").argtypes = [p, p, i64, p, p] + [p] * 7 + [i32]
             getattr(_lib, f"tco_hybrid_{sfx}").argtypes = [p, p, i64, p, p, p] + [p] * 8 + [i32]
             getattr(_lib, f"tco_closest_point_triangle_{sfx}").argtypes = [p, p, i64, p, p, i32]
-            getattr(_lib, f"tco_degenerate_{sfx}").argtypes = [p, i64, p, i32]
+            getattr(_lib, f"tco_degenerate_{sfx}").argtypes = [p, i64, ctypes.c_double, p, i32]
             getattr(_lib, f"tco_margins_{sfx}").argtypes = [p, p, i64, p, p, p, i32]
             getattr(_lib, f"tco_apply_motion_{sfx}").argtypes = [p, i64, p, p, p]
             for name in ("comparison", "iterative", "hybrid", "closest_point_triangle", "degenerate", "margins",
@@ -190,10 +190,10 @@ def closest_point_triangle(P, T, dtype=np.float64, threads=1):
     return c, b
 
 
-def degenerate(T, dtype=np.float64, threads=1):
+def degenerate(T, dtype=np.float64, threads=1, rel_tol=1e-12):
     T = _tris(T, dtype)
     m = np.empty(T.shape[0], np.uint8)
-    rc = getattr(lib(), f"tco_degenerate_{_sfx(dtype)}")(_ptr(T), T.shape[0], _ptr(m), threads)
+    rc = getattr(lib(), f"tco_degenerate_{_sfx(dtype)}")(_ptr(T), T.shape[0], float(rel_tol), _ptr(m), threads)
     assert rc == 0
     return m.astype(bool)
 

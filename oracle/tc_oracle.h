@@ -45,7 +45,7 @@ typedef struct {
                          int8_t* kind, uint8_t* ids, int64_t* counts, int threads);      \
     int tco_closest_point_triangle_##SFX(const REAL* P, const REAL* T, int64_t n,        \
                                          REAL* closest, REAL* bary, int threads);        \
-    int tco_degenerate_##SFX(const REAL* T, int64_t n, uint8_t* mask, int threads);              \
+    int tco_degenerate_##SFX(const REAL* T, int64_t n, double rel_tol, uint8_t* mask, int threads);              \
     int tco_apply_motion_##SFX(const REAL* points, int64_t n, const double* quat, const REAL* t, \
                                REAL* out);                                                    \
     int tco_margins_##SFX(const REAL* A, const REAL* B, int64_t n, const REAL* eps,              \

@@ -58,8 +58,9 @@ static inline double FN(fabsd_)(double x) { return x < 0 ? -x : x; }
 static inline double FN(mind_)(double a, double b) { return a < b ? a : b; }
 static inline double FN(max_d_)(double a, double b) { return a > b ? a : b; }
 
-/* RK/geometry.py:68-75 degenerate_mask (rel_tol = 1e-12). */
-static int FN(degenerate_one_)(const REAL* t) {
+/* RK/geometry.py:68-75 degenerate_mask: sq_area < rel_tol * L * L, rel_tol
+ * rounded to REAL like the reference's Python float times a REAL array. */
+static int FN(degenerate_tol_one_)(const REAL* t, double rel_tol) {
     REAL e1[3], e2[3], c[3], ed[3];
     FN(sub3_)(t + 3, t, e1);
     FN(sub3_)(t + 6, t, e2);
@@ -71,10 +72,13 @@ static int FN(degenerate_one_)(const REAL* t) {
     FN(sub3_)(t + 6, t + 3, ed); l1 = FN(dot3_)(ed, ed);
     FN(sub3_)(t, t + 6, ed); l2 = FN(dot3_)(ed, ed);
     L = FN(max_)(FN(max_)(l0, l1), l2);
-    REAL thr = (REAL)1e-12 * L;
+    REAL thr = (REAL)rel_tol * L;
     thr = thr * L;
     return (L == (REAL)0) || (sq_area < thr);
 }
+
+/* the hybrid's screen uses the reference default (RK/kernels.py:598) */
+static int FN(degenerate_one_)(const REAL* t) { return FN(degenerate_tol_one_)(t, 1e-12); }
 
 /* RK/kernels.py:157-221 closest_point_triangle_batch, one point.
  * Returns the region claimed, in claim order: 0 VA, 1 VB, 2 EAB, 3 VC,
@@ -582,6 +586,7 @@ typedef struct {
     int8_t* kind;
     uint8_t* ids;
     int64_t n_fb[TCO_MAX_THREADS], n_deg[TCO_MAX_THREADS];
+    double rel_tol;
 } FN(ctx_);
 
 static void FN(comparison_body_)(int64_t lo, int64_t hi, int tid, void* arg) {
@@ -660,7 +665,7 @@ static void FN(cpt_body_)(int64_t lo, int64_t hi, int tid, void* arg) {
 static void FN(degenerate_body_)(int64_t lo, int64_t hi, int tid, void* arg) {
     FN(ctx_)* c = (FN(ctx_)*)arg;
     (void)tid;
-    for (int64_t i = lo; i < hi; ++i) c->ids[i] = (uint8_t)FN(degenerate_one_)(c->A + 9 * i);
+    for (int64_t i = lo; i < hi; ++i) c->ids[i] = (uint8_t)FN(degenerate_tol_one_)(c->A + 9 * i, c->rel_tol);
 }
 
 int FN(tco_comparison_)(const REAL* A, const REAL* B, int64_t n, const REAL* eps,
@@ -738,10 +743,10 @@ int FN(tco_closest_point_triangle_)(const REAL* P, const REAL* T, int64_t n, REA
     return 0;
 }
 
-int FN(tco_degenerate_)(const REAL* T, int64_t n, uint8_t* mask, int threads) {
+int FN(tco_degenerate_)(const REAL* T, int64_t n, double rel_tol, uint8_t* mask, int threads) {
     if (n < 0 || (n > 0 && (!T || !mask))) return 1;
     FN(ctx_) c = {0};
-    c.A = T; c.ids = mask;
+    c.A = T; c.ids = mask; c.rel_tol = rel_tol;
     tco_parallel_for(n, threads, FN(degenerate_body_), &c);
     return 0;
 }

@@ -14,6 +14,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libtricontact_b200.so"
 
+TC_ABI_VERSION = 2  # include/tricontact_b200.h
 TC_OK, TC_EINVAL, TC_EDEGENERATE, TC_ECUDA, TC_ENODEVICE = 0, 1, 2, 3, 4
 TC_SOA, TC_STRICT, TC_EMIT_IDS = 1, 2, 4
 VARIANTS = {"comparison": 0, "iterative": 1, "hybrid": 2}
@@ -64,12 +65,12 @@ SIGNATURES = {
     "tc_closest_point_triangle_f32": (_INT, [_P, _P, _I64, _P, _P, _P]),
     "tc_point_triangle_distance_f64": (_INT, [_P, _P, _I64, _P, _I64, _P, _P, _P]),
     "tc_point_triangle_distance_f32": (_INT, [_P, _P, _I64, _P, _I64, _P, _P, _P]),
-    "tc_degenerate_mask_f64": (_INT, [_P, _I64, _P, _P]),
-    "tc_degenerate_mask_f32": (_INT, [_P, _I64, _P, _P]),
+    "tc_degenerate_mask_f64": (_INT, [_P, _I64, ctypes.c_double, _P, _P]),
+    "tc_degenerate_mask_f32": (_INT, [_P, _I64, ctypes.c_double, _P, _P]),
     "tc_closest_point_triangle_host_f64": (_INT, [_P, _P, _I64, _P, _P]),
     "tc_closest_point_triangle_host_f32": (_INT, [_P, _P, _I64, _P, _P]),
-    "tc_degenerate_mask_host_f64": (_INT, [_P, _I64, _P]),
-    "tc_degenerate_mask_host_f32": (_INT, [_P, _I64, _P]),
+    "tc_degenerate_mask_host_f64": (_INT, [_P, _I64, ctypes.c_double, _P]),
+    "tc_degenerate_mask_host_f32": (_INT, [_P, _I64, ctypes.c_double, _P]),
     "tc_run_host_f64": (_INT, [_INT, _P, _P, _I64, _P, _P, _P] + [_P] * 7 + [_P]),
     "tc_run_host_f32": (_INT, [_INT, _P, _P, _I64, _P, _P, _P] + [_P] * 7 + [_P]),
 }
@@ -113,6 +114,9 @@ def load(path: Path | str | None = None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.tc_abi_version() != TC_ABI_VERSION:
+        raise TricontactError(f"{p} implements ABI {lib.tc_abi_version()}, this binding expects {TC_ABI_VERSION}: "
+                              "rebuild it with `python -m paper_2105_12415_b200._build`")
     if path is None:
         _lib = lib
     return lib

@@ -30,6 +30,9 @@
 #include <cub/device/device_scan.cuh>
 #include <vector>
 #include <mutex>
+#include <condition_variable>
+#include <memory>
+#include <thread>
 #include <dlfcn.h>
 #if __has_include(<nccl.h>)
 #include <nccl.h>  // types only: libnccl.so.2 is dlopen'ed on first use (tc_allreduce_stats)
@@ -1043,13 +1046,13 @@ __global__ void __launch_bounds__(BLOCK) ptd_kernel(const T* P, const T* Tr, con
 }
 
 template <typename T>
-__global__ void __launch_bounds__(BLOCK) degenerate_kernel(const T* Tr, int64_t n, uint8_t* mask) {
+__global__ void __launch_bounds__(BLOCK) degenerate_kernel(const T* Tr, int64_t n, double rel_tol, uint8_t* mask) {
     using R = Strict<T>;
     for (int64_t i = (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
         R t[9];
 #pragma unroll
         for (int k = 0; k < 9; ++k) t[k] = R(Tr[9 * i + k]);
-        mask[i] = degenerate_tri(t) ? 1 : 0;
+        mask[i] = degenerate_tri(t, rel_tol) ? 1 : 0;
     }
 }
 
@@ -1082,15 +1085,26 @@ __global__ void stats_reset_kernel(tc_stats* s) {
 }
 
 // ---- launch helpers ------------------------------------------------------------------
+// Per-device state is keyed by the calling thread's current device
+// (cudaGetDevice), so one process can drive several GPUs through the same
+// entry points.
+constexpr int kMaxDevices = 64;
+
+static int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    return dev;
+}
+
 static int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+    static std::atomic<int> sms[kMaxDevices];
+    const int dev = current_device();
+    int v = sms[dev].load(std::memory_order_relaxed);
+    if (!v) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        sms[dev].store(v, std::memory_order_relaxed);
     }
-    return sms;
+    return v;
 }
 
 template <typename K>
@@ -1115,11 +1129,11 @@ enum Variant { V_COMPARISON = 0, V_ITERATIVE = 1, V_HYBRID = 2 };
 // pool; raising its release threshold once keeps freed blocks cached between
 // calls, so per-call workspaces cost no cudaMalloc/cudaFree synchronisation.
 static void pool_init() {
-    static std::once_flag pool_once;
-    std::call_once(pool_once, [] {
-        int dev = 0;
+    static std::once_flag pool_once[kMaxDevices];
+    const int dev = current_device();
+    std::call_once(pool_once[dev], [dev] {
         cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t keep = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
@@ -1368,19 +1382,163 @@ static int run_multiscale(const T* tris, const int32_t* owner, const T* motions,
 }
 
 // ---- host pipeline ----------------------------------------------------------------------
-// Chunks of the pair range are staged through per-stream device buffers:
-// H2D(c) on stream c % NS, then the kernel, then D2H -- so the copies of one
-// chunk overlap the kernel of its neighbours.
+// tc_run_host_*: the pair range is processed in chunks on NS streams; chunk c
+// uses slot c % NS -- H2D of its inputs, the kernel, D2H of its outputs -- so
+// the copies of one chunk overlap the kernels and copies of its neighbours.
+//
+// Caller arrays may be pinned (cudaHostAlloc / cudaHostRegister: the DMA
+// engines read and write them directly) or pageable, like the drop-in's numpy
+// arrays.  cudaMemcpyAsync on pageable memory goes through the driver's
+// bounce buffer synchronously and would serialise the pipeline, so each
+// pageable array is staged through the slot's own pinned buffers by a pool of
+// host threads: the inputs of chunk c are copied in while the GPU works on the
+// chunks before it, and the results of chunk c - NS are copied out to the
+// caller before its slot is reused.
+
+struct CopyPiece {
+    char* dst;
+    const char* src;
+    size_t bytes;
+};
+
+// Parallel memcpy on persistent host threads (the caller takes part).
+class CopyPool {
+  public:
+    explicit CopyPool(int workers) {
+        for (int i = 0; i < workers; ++i) th_.emplace_back([this] { worker(); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void copy(const std::vector<CopyPiece>& segs) {
+        size_t total = 0;
+        for (const auto& sg : segs) total += sg.bytes;
+        if (!total) return;
+        const size_t parts = th_.size() + 1;
+        const size_t piece = std::max<size_t>(total / (2 * parts) + 1, size_t(1) << 20);
+        std::vector<CopyPiece> local;
+        for (const auto& sg : segs)
+            for (size_t o = 0; o < sg.bytes; o += piece)
+                local.push_back({sg.dst + o, sg.src + o, std::min(piece, sg.bytes - o)});
+        if (th_.empty() || local.size() == 1) {
+            for (const auto& pc : local) memcpy(pc.dst, pc.src, pc.bytes);
+            return;
+        }
+        {
+            // no worker may still be inside drain() of the previous generation
+            std::unique_lock<std::mutex> l(mu_);
+            done_cv_.wait(l, [this] { return active_ == 0; });
+            pieces_.swap(local);
+            next_.store(0);
+            left_.store(pieces_.size());
+            ++gen_;
+            ++active_;
+        }
+        cv_.notify_all();
+        drain();
+        std::unique_lock<std::mutex> l(mu_);
+        --active_;
+        done_cv_.notify_all();
+        done_cv_.wait(l, [this] { return left_.load() == 0; });
+    }
+
+  private:
+    void drain() {
+        for (;;) {
+            const size_t i = next_.fetch_add(1);
+            if (i >= pieces_.size()) break;
+            memcpy(pieces_[i].dst, pieces_[i].src, pieces_[i].bytes);
+            if (left_.fetch_sub(1) == 1) {
+                std::lock_guard<std::mutex> l(mu_);
+                done_cv_.notify_all();
+            }
+        }
+    }
+    void worker() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> l(mu_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                ++active_;
+            }
+            drain();
+            {
+                std::lock_guard<std::mutex> l(mu_);
+                --active_;
+            }
+            done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::vector<CopyPiece> pieces_;
+    std::atomic<size_t> next_{0}, left_{0};
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    uint64_t gen_ = 0;
+    int active_ = 0;
+    bool stop_ = false;
+};
+
+struct HostSlot {
+    cudaStream_t st = nullptr;
+    cudaEvent_t done = nullptr;
+    void* dbuf = nullptr;   // device chunk buffers
+    size_t dcap = 0;
+    char* hin = nullptr;    // pinned staging of pageable inputs
+    size_t hin_cap = 0;
+    char* hout = nullptr;   // pinned staging of pageable outputs
+    size_t hout_cap = 0;
+    bool busy = false;      // work enqueued since the last finish
+    std::vector<CopyPiece> out;  // staged results to copy to the caller
+};
+
 struct HostCtx {
     static constexpr int NS = 3;
     std::mutex mu;
     bool init = false;
-    cudaStream_t st[NS];
-    void* buf[NS] = {nullptr, nullptr, nullptr};
-    size_t cap = 0;
+    HostSlot slot[NS];
     tc_stats* dstats = nullptr;
+    std::unique_ptr<CopyPool> pool;
 };
-static HostCtx g_host;
+static HostCtx g_host[kMaxDevices];  // one per device (current device of the calling thread)
+
+static bool host_pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();  // unregistered host memory on older runtimes: clear the error
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged;
+}
+
+static cudaError_t grow_pinned(char*& buf, size_t& cap, size_t need) {
+    if (need <= cap) return cudaSuccess;
+    if (buf) cudaFreeHost(buf);
+    buf = nullptr;
+    cap = 0;
+    const cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&buf), need, cudaHostAllocDefault);
+    if (e == cudaSuccess) cap = need;
+    return e;
+}
+
+// Wait for a slot's work and copy its staged results to the caller.
+static cudaError_t finish_slot(HostCtx& h, HostSlot& S) {
+    if (!S.busy) return cudaSuccess;
+    const cudaError_t e = cudaEventSynchronize(S.done);
+    if (e == cudaSuccess) h.pool->copy(S.out);
+    S.out.clear();
+    S.busy = false;
+    return e;
+}
 
 template <typename T>
 static int run_host(int variant, const T* tri_a, const T* tri_b, int64_t n, const T* eps, const uint8_t* allow,
@@ -1394,87 +1552,143 @@ static int run_host(int variant, const T* tri_a, const T* tri_b, int64_t n, cons
         snprintf(g_err, sizeof(g_err), "host entry points take the (n,3,3) layout only");
         return TC_EINVAL;
     }
-    std::lock_guard<std::mutex> lock(g_host.mu);
-    HostCtx& h = g_host;
+    HostCtx& h = g_host[current_device()];
+    std::lock_guard<std::mutex> lock(h.mu);
     cudaError_t e;
     if (!h.init) {
-        for (int k = 0; k < HostCtx::NS; ++k)
-            if ((e = cudaStreamCreateWithFlags(&h.st[k], cudaStreamNonBlocking)) != cudaSuccess)
+        for (auto& S : h.slot) {
+            if ((e = cudaStreamCreateWithFlags(&S.st, cudaStreamNonBlocking)) != cudaSuccess)
                 return set_err("cudaStreamCreate", e);
+            if ((e = cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming)) != cudaSuccess)
+                return set_err("cudaEventCreate", e);
+        }
         if ((e = cudaMalloc(&h.dstats, sizeof(tc_stats))) != cudaSuccess) return set_err("cudaMalloc", e);
+        const char* v = getenv("TC_HOST_THREADS");  // host copy threads (pageable staging)
+        const int hw = (int)std::thread::hardware_concurrency();
+        const int nt = v ? atoi(v) : std::min(std::max(hw, 1), 16);
+        h.pool.reset(new CopyPool(std::max(nt, 1) - 1));
         h.init = true;
     }
-    static const int64_t chunk = [] {
-        const char* v = getenv("TC_HOST_CHUNK");  // pairs per pipeline chunk (tuning knob)
+    // pairs per pipeline chunk: n / 8 within [64K, 1M] so a call pipelines
+    // (TC_HOST_CHUNK overrides)
+    int64_t chunk;
+    {
+        const char* v = getenv("TC_HOST_CHUNK");
         const long long c = v ? atoll(v) : 0;
-        return (int64_t)(c >= 4096 ? c : (1 << 20));
-    }();
-    const bool want_ids = (p->flags & TC_EMIT_IDS) && ids;
-    // per-pair bytes staged: inputs, eps, allow, outputs
-    const size_t per = sizeof(T) * (18 + 1 + 11) + 2 + (want_ids ? 4 : 0);
-    const size_t need = per * (size_t)(n < chunk ? (n > 0 ? n : 1) : chunk) + 256 * 16;
-    if (need > h.cap) {
-        for (int k = 0; k < HostCtx::NS; ++k) {
-            if (h.buf[k]) cudaFree(h.buf[k]);
-            h.buf[k] = nullptr;
-            if ((e = cudaMalloc(&h.buf[k], need)) != cudaSuccess) {
-                h.cap = 0;
-                return set_err("cudaMalloc", e);
-            }
-        }
-        h.cap = need;
+        chunk = c >= 4096 ? (int64_t)c : std::min<int64_t>(int64_t(1) << 20, std::max<int64_t>(65536, n / 8));
+        chunk = (chunk + 4095) & ~int64_t(4095);
     }
-    stats_reset_kernel<<<1, 1, 0, h.st[0]>>>(h.dstats);
+    const bool want_ids = (p->flags & TC_EMIT_IDS) && ids;
+    // which caller arrays are pageable (staged) and the staging bytes per pair
+    struct Arr {
+        const void* src;  // caller array (input or output)
+        size_t per;       // bytes per pair
+        bool staged;
+    };
+    Arr in[4] = {{tri_a, 9 * sizeof(T), false}, {tri_b, 9 * sizeof(T), false}, {eps, sizeof(T), false},
+                 {allow, 1, false}};
+    Arr out[7] = {{distance, sizeof(T), false}, {pa, 3 * sizeof(T), false}, {pb, 3 * sizeof(T), false},
+                  {ba, 2 * sizeof(T), false}, {bb, 2 * sizeof(T), false}, {kind, 1, false},
+                  {want_ids ? ids : nullptr, 4, false}};
+    size_t in_per = 0, out_per = 0, dev_per = 0;
+    for (auto& a : in) {
+        if (!a.src) continue;
+        a.staged = !host_pinned(a.src);
+        if (a.staged) in_per += a.per;
+        dev_per += a.per;
+    }
+    for (auto& a : out) {
+        if (!a.src) continue;
+        a.staged = !host_pinned(a.src);
+        if (a.staged) out_per += a.per;
+        dev_per += a.per;
+    }
+    const int64_t cmax = n < chunk ? (n > 0 ? n : 1) : chunk;
+    const size_t slack = 256 * 16;  // 256-byte alignment of every carved array
+    for (auto& S : h.slot) {
+        const size_t need = dev_per * (size_t)cmax + slack;
+        if (need > S.dcap) {
+            if (S.dbuf) cudaFree(S.dbuf);
+            S.dbuf = nullptr;
+            S.dcap = 0;
+            if ((e = cudaMalloc(&S.dbuf, need)) != cudaSuccess) return set_err("cudaMalloc", e);
+            S.dcap = need;
+        }
+        if (in_per && (e = grow_pinned(S.hin, S.hin_cap, in_per * (size_t)cmax + slack)) != cudaSuccess)
+            return set_err("cudaHostAlloc", e);
+        if (out_per && (e = grow_pinned(S.hout, S.hout_cap, out_per * (size_t)cmax + slack)) != cudaSuccess)
+            return set_err("cudaHostAlloc", e);
+    }
+    cudaStream_t s0 = h.slot[0].st;
+    stats_reset_kernel<<<1, 1, 0, s0>>>(h.dstats);
     g_launches++;
-    cudaEvent_t ready;
-    cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
-    cudaEventRecord(ready, h.st[0]);
-    for (int k = 1; k < HostCtx::NS; ++k) cudaStreamWaitEvent(h.st[k], ready, 0);
+    cudaEventRecord(h.slot[0].done, s0);
+    for (int k = 1; k < HostCtx::NS; ++k) cudaStreamWaitEvent(h.slot[k].st, h.slot[0].done, 0);
     int rc = TC_OK;
+    cudaError_t herr = cudaSuccess;
     for (int64_t c0 = 0, ci = 0; c0 < n && rc == TC_OK; c0 += chunk, ++ci) {
         const int64_t m = (n - c0) < chunk ? (n - c0) : chunk;
-        const int k = (int)(ci % HostCtx::NS);
-        cudaStream_t s = h.st[k];
-        char* base = static_cast<char*>(h.buf[k]);
-        auto carve = [&](size_t bytes) { char* r = base; base += (bytes + 255) & ~size_t(255); return r; };
-        T* dA = (T*)carve(sizeof(T) * 9 * m);
-        T* dB = (T*)carve(sizeof(T) * 9 * m);
-        T* dE = eps ? (T*)carve(sizeof(T) * m) : nullptr;
-        uint8_t* dF = allow ? (uint8_t*)carve(m) : nullptr;
-        T* dD = distance ? (T*)carve(sizeof(T) * m) : nullptr;
-        T* dPA = pa ? (T*)carve(sizeof(T) * 3 * m) : nullptr;
-        T* dPB = pb ? (T*)carve(sizeof(T) * 3 * m) : nullptr;
-        T* dBA = ba ? (T*)carve(sizeof(T) * 2 * m) : nullptr;
-        T* dBB = bb ? (T*)carve(sizeof(T) * 2 * m) : nullptr;
-        int8_t* dK = kind ? (int8_t*)carve(m) : nullptr;
-        uint8_t* dI = want_ids ? (uint8_t*)carve(4 * m) : nullptr;
-        cudaMemcpyAsync(dA, tri_a + 9 * c0, sizeof(T) * 9 * m, cudaMemcpyHostToDevice, s);
-        cudaMemcpyAsync(dB, tri_b + 9 * c0, sizeof(T) * 9 * m, cudaMemcpyHostToDevice, s);
-        if (dE) cudaMemcpyAsync(dE, eps + c0, sizeof(T) * m, cudaMemcpyHostToDevice, s);
-        if (dF) cudaMemcpyAsync(dF, allow + c0, m, cudaMemcpyHostToDevice, s);
-        rc = run_device<T>(variant, dA, dB, m, dE, dF, p, dD, dPA, dPB, dBA, dBB, dK, dI, h.dstats, s);
-        if (dD) cudaMemcpyAsync(distance + c0, dD, sizeof(T) * m, cudaMemcpyDeviceToHost, s);
-        if (dPA) cudaMemcpyAsync(pa + 3 * c0, dPA, sizeof(T) * 3 * m, cudaMemcpyDeviceToHost, s);
-        if (dPB) cudaMemcpyAsync(pb + 3 * c0, dPB, sizeof(T) * 3 * m, cudaMemcpyDeviceToHost, s);
-        if (dBA) cudaMemcpyAsync(ba + 2 * c0, dBA, sizeof(T) * 2 * m, cudaMemcpyDeviceToHost, s);
-        if (dBB) cudaMemcpyAsync(bb + 2 * c0, dBB, sizeof(T) * 2 * m, cudaMemcpyDeviceToHost, s);
-        if (dK) cudaMemcpyAsync(kind + c0, dK, m, cudaMemcpyDeviceToHost, s);
-        if (dI) cudaMemcpyAsync(ids + 4 * c0, dI, 4 * m, cudaMemcpyDeviceToHost, s);
+        HostSlot& S = h.slot[ci % HostCtx::NS];
+        // the slot's staging buffers are free once its previous chunk is done
+        if ((e = finish_slot(h, S)) != cudaSuccess) {
+            herr = e;
+            break;
+        }
+        cudaStream_t s = S.st;
+        char* dbase = static_cast<char*>(S.dbuf);
+        char* ibase = S.hin;
+        char* obase = S.hout;
+        auto carve = [](char*& b, size_t bytes) {
+            char* r = b;
+            b += (bytes + 255) & ~size_t(255);
+            return r;
+        };
+        void* dptr[4] = {nullptr, nullptr, nullptr, nullptr};
+        const char* hsrc[4] = {nullptr, nullptr, nullptr, nullptr};
+        std::vector<CopyPiece> stage_in;
+        for (int k = 0; k < 4; ++k) {
+            if (!in[k].src) continue;
+            const size_t bytes = in[k].per * (size_t)m;
+            hsrc[k] = static_cast<const char*>(in[k].src) + in[k].per * (size_t)c0;
+            dptr[k] = carve(dbase, bytes);
+            if (in[k].staged) {
+                char* st = carve(ibase, bytes);
+                stage_in.push_back({st, hsrc[k], bytes});
+                hsrc[k] = st;
+            }
+        }
+        h.pool->copy(stage_in);  // fill the pinned staging before its DMA is enqueued
+        for (int k = 0; k < 4; ++k)
+            if (dptr[k]) cudaMemcpyAsync(dptr[k], hsrc[k], in[k].per * (size_t)m, cudaMemcpyHostToDevice, s);
+        void* optr[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        for (int k = 0; k < 7; ++k)
+            if (out[k].src) optr[k] = carve(dbase, out[k].per * (size_t)m);
+        rc = run_device<T>(variant, (const T*)dptr[0], (const T*)dptr[1], m, (const T*)dptr[2],
+                           (const uint8_t*)dptr[3], p, (T*)optr[0], (T*)optr[1], (T*)optr[2], (T*)optr[3],
+                           (T*)optr[4], (int8_t*)optr[5], (uint8_t*)optr[6], h.dstats, s);
+        for (int k = 0; k < 7; ++k) {
+            if (!out[k].src) continue;
+            const size_t bytes = out[k].per * (size_t)m;
+            char* dst = static_cast<char*>(const_cast<void*>(out[k].src)) + out[k].per * (size_t)c0;
+            if (out[k].staged) {
+                char* st = carve(obase, bytes);
+                S.out.push_back({dst, st, bytes});
+                dst = st;
+            }
+            cudaMemcpyAsync(dst, optr[k], bytes, cudaMemcpyDeviceToHost, s);
+        }
+        cudaEventRecord(S.done, s);
+        S.busy = true;
+    }
+    for (auto& S : h.slot) {
+        e = finish_slot(h, S);
+        if (herr == cudaSuccess) herr = e;
     }
     tc_stats hs;
-    for (int k = 1; k < HostCtx::NS; ++k) {
-        cudaEventRecord(ready, h.st[k]);
-        cudaStreamWaitEvent(h.st[0], ready, 0);
-    }
-    cudaMemcpyAsync(&hs, h.dstats, sizeof(tc_stats), cudaMemcpyDeviceToHost, h.st[0]);
-    e = cudaStreamSynchronize(h.st[0]);
-    for (int k = 1; k < HostCtx::NS; ++k) {
-        const cudaError_t e2 = cudaStreamSynchronize(h.st[k]);
-        if (e == cudaSuccess) e = e2;
-    }
-    cudaEventDestroy(ready);
+    cudaMemcpy(&hs, h.dstats, sizeof(tc_stats), cudaMemcpyDeviceToHost);  // after every slot is done
     if (rc != TC_OK) return rc;
-    if (e != cudaSuccess) return set_err("host pipeline", e);
+    if (herr == cudaSuccess) herr = cudaGetLastError();
+    if (herr != cudaSuccess) return set_err("host pipeline", herr);
     if (stats) {
         stats->iterative += hs.iterative;
         stats->comparison += hs.comparison;
@@ -1516,11 +1730,11 @@ static int run_ptd(const T* P, const T* Tr, int64_t n_tris, const int32_t* tri_i
 }
 
 template <typename T>
-static int run_degenerate(const T* Tr, int64_t n, uint8_t* mask, void* stream) {
+static int run_degenerate(const T* Tr, int64_t n, double rel_tol, uint8_t* mask, void* stream) {
     if (n < 0 || (n > 0 && (!Tr || !mask))) return TC_EINVAL;
     if (n == 0) return TC_OK;
     auto k = degenerate_kernel<T>;
-    k<<<(unsigned)grid_for(k, n), BLOCK, 0, reinterpret_cast<cudaStream_t>(stream)>>>(Tr, n, mask);
+    k<<<(unsigned)grid_for(k, n), BLOCK, 0, reinterpret_cast<cudaStream_t>(stream)>>>(Tr, n, rel_tol, mask);
     g_launches++;
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TC_OK : set_err("degenerate launch", e);
@@ -1553,7 +1767,7 @@ static int run_cpt_host(const T* P, const T* Tr, int64_t n, T* closest, T* bary)
 }
 
 template <typename T>
-static int run_degenerate_host(const T* Tr, int64_t n, uint8_t* mask) {
+static int run_degenerate_host(const T* Tr, int64_t n, double rel_tol, uint8_t* mask) {
     if (n < 0 || (n > 0 && (!Tr || !mask))) return TC_EINVAL;
     if (n == 0) return TC_OK;
     char* d = nullptr;
@@ -1562,7 +1776,7 @@ static int run_degenerate_host(const T* Tr, int64_t n, uint8_t* mask) {
     T* dT = (T*)d;
     uint8_t* dM = (uint8_t*)(dT + 9 * n);
     cudaMemcpy(dT, Tr, sizeof(T) * 9 * n, cudaMemcpyHostToDevice);
-    int rc = run_degenerate<T>(dT, n, dM, nullptr);
+    int rc = run_degenerate<T>(dT, n, rel_tol, dM, nullptr);
     if (rc == TC_OK) {
         cudaMemcpy(mask, dM, n, cudaMemcpyDeviceToHost);
         e = cudaDeviceSynchronize();
@@ -1714,11 +1928,11 @@ int tc_point_triangle_distance_f32(const float* points, const float* tris, int64
                                    int64_t n, float* distance, float* closest, void* stream) {
     return tc::run_ptd<float>(points, tris, n_tris, tri_index, n, distance, closest, stream);
 }
-int tc_degenerate_mask_f64(const double* tris, int64_t n, uint8_t* mask, void* stream) {
-    return tc::run_degenerate<double>(tris, n, mask, stream);
+int tc_degenerate_mask_f64(const double* tris, int64_t n, double rel_tol, uint8_t* mask, void* stream) {
+    return tc::run_degenerate<double>(tris, n, rel_tol, mask, stream);
 }
-int tc_degenerate_mask_f32(const float* tris, int64_t n, uint8_t* mask, void* stream) {
-    return tc::run_degenerate<float>(tris, n, mask, stream);
+int tc_degenerate_mask_f32(const float* tris, int64_t n, double rel_tol, uint8_t* mask, void* stream) {
+    return tc::run_degenerate<float>(tris, n, rel_tol, mask, stream);
 }
 
 int tc_closest_point_triangle_host_f64(const double* points, const double* tris, int64_t n, double* closest,
@@ -1729,11 +1943,11 @@ int tc_closest_point_triangle_host_f32(const float* points, const float* tris, i
                                        float* bary) {
     return tc::run_cpt_host<float>(points, tris, n, closest, bary);
 }
-int tc_degenerate_mask_host_f64(const double* tris, int64_t n, uint8_t* mask) {
-    return tc::run_degenerate_host<double>(tris, n, mask);
+int tc_degenerate_mask_host_f64(const double* tris, int64_t n, double rel_tol, uint8_t* mask) {
+    return tc::run_degenerate_host<double>(tris, n, rel_tol, mask);
 }
-int tc_degenerate_mask_host_f32(const float* tris, int64_t n, uint8_t* mask) {
-    return tc::run_degenerate_host<float>(tris, n, mask);
+int tc_degenerate_mask_host_f32(const float* tris, int64_t n, double rel_tol, uint8_t* mask) {
+    return tc::run_degenerate_host<float>(tris, n, rel_tol, mask);
 }
 
 int tc_blocks_hybrid_f64(const double* meshes, int32_t tris_per_mesh, int64_t n_meshes,

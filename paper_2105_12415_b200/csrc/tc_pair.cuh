@@ -70,9 +70,11 @@ __device__ __forceinline__ R max_sq_edge(const R* t) {
     return maxv(maxv(l0, l1), l2);
 }
 
-// RK/geometry.py:68-75 degenerate_mask, rel_tol = 1e-12
+// RK/geometry.py:68-75 degenerate_mask: sq_area < rel_tol * L * L, with
+// rel_tol rounded to T like the reference's Python float times a T array
+// (the hybrid's fallback screen uses the default 1e-12, RK/kernels.py:598)
 template <class R>
-__device__ __forceinline__ bool degenerate_tri(const R* t) {
+__device__ __forceinline__ bool degenerate_tri(const R* t, double rel_tol = 1e-12) {
     using T = typename Store<R>::type;
     R e1[3], e2[3], c[3];
     sub3(t + 3, t, e1);
@@ -80,7 +82,7 @@ __device__ __forceinline__ bool degenerate_tri(const R* t) {
     cross3(e1, e2, c);
     R sq_area = R(T(0.25)) * dot3(c, c);
     R L = max_sq_edge(t);
-    R thr = R(T(1e-12)) * L;
+    R thr = R(T(rel_tol)) * L;
     thr = thr * L;
     return (L == R(0)) || (sq_area < thr);
 }

@@ -181,14 +181,21 @@ def _sfx(dtype) -> str:
 
 
 def _run(variant: str, A, B, eps, params, allow=None):
-    """One host-buffer C-ABI call; returns (BatchResult, TcStats, rc)."""
+    """One host-buffer C-ABI call; returns (BatchResult, TcStats, rc).
+
+    ``eps`` is the reference's per-pair halo array, or a positive scalar,
+    which travels as ``tc_params.epsilon`` instead of an (n,) array (the
+    kernels read ``eps == NULL`` as "every pair uses params.epsilon", rounded
+    to REAL exactly like ``np.asarray(eps, REAL)``).  ``allow``: an (n,) mask,
+    already broadcast by the caller.  Pageable numpy buffers are staged through
+    the library's pinned buffers (tc_run_host_*, include/tricontact_b200.h).
+    """
     lib = _abi.load()
     A = np.ascontiguousarray(A, dtype=REAL)
     B = np.ascontiguousarray(B, dtype=REAL)
     n = A.shape[0]
     if B.shape[0] != n:
         raise ValueError("tri_a and tri_b must have the same length")
-    eps = np.ascontiguousarray(eps, dtype=REAL)
     res = BatchResult(
         kind=np.empty(n, np.int8),
         distance=np.empty(n, REAL),
@@ -201,15 +208,33 @@ def _run(variant: str, A, B, eps, params, allow=None):
     if n == 0:
         return res, stats, _abi.TC_OK
     p = _abi.params_struct(params if params is not None else KernelParams(), _flags())
+    eps_arr = None
+    if np.ndim(eps) == 0 and float(eps) > 0.0:
+        p.epsilon = float(eps)
+    else:
+        eps_arr = np.ascontiguousarray(np.broadcast_to(np.asarray(eps, dtype=REAL), (n,)))
     if allow is not None:
         allow = np.ascontiguousarray(allow, dtype=np.uint8)
+        if allow.shape != (n,):
+            raise ValueError("allow_fallback mask must have shape (n,)")
     fn = getattr(lib, f"tc_run_host_{_sfx(REAL)}")
-    rc = fn(_abi.VARIANTS[variant], _ptr(A), _ptr(B), n, _ptr(eps), _ptr(allow), ctypes.byref(p),
+    rc = fn(_abi.VARIANTS[variant], _ptr(A), _ptr(B), n, _ptr(eps_arr), _ptr(allow), ctypes.byref(p),
             _ptr(res.distance), _ptr(res.point_a), _ptr(res.point_b), _ptr(res.bary_a), _ptr(res.bary_b),
             _ptr(res.kind), None, ctypes.byref(stats))
     if rc not in (_abi.TC_OK, _abi.TC_EDEGENERATE):
         _abi.check(rc, f"tc_run_host ({variant})")
     return res, stats, rc
+
+
+def _halo(eps, n: int):
+    """RK/kernels.py:143-149 _as_eps, keeping a scalar halo scalar (same
+    validation and rounding; the kernels broadcast it)."""
+    e = np.asarray(eps, dtype=REAL)
+    if e.ndim == 0:
+        return e
+    if e.shape != (n,):
+        raise ValueError("eps must be scalar or shape (n,)")
+    return e
 
 
 # ---------------------------------------------------------------------------
@@ -235,13 +260,12 @@ def closest_point_triangle_batch(points: np.ndarray, tris: np.ndarray):
 
 
 def degenerate_mask(tris: np.ndarray, rel_tol: float = 1e-12) -> np.ndarray:
-    """RK/geometry.py:68-75 (the kernel implements the default rel_tol only)."""
-    if rel_tol != 1e-12:
-        raise ValueError("the device degenerate test is compiled for rel_tol=1e-12")
+    """RK/geometry.py:68-75: squared area below ``rel_tol * longest_edge**4``."""
     t = np.ascontiguousarray(as_triangles(tris))
     mask = np.zeros(t.shape[0], np.uint8)
     if t.shape[0]:
-        rc = getattr(_abi.load(), f"tc_degenerate_mask_host_{_sfx(REAL)}")(_ptr(t), t.shape[0], _ptr(mask))
+        rc = getattr(_abi.load(), f"tc_degenerate_mask_host_{_sfx(REAL)}")(_ptr(t), t.shape[0], float(rel_tol),
+                                                                          _ptr(mask))
         _abi.check(rc, "tc_degenerate_mask_host")
     return mask.astype(bool)
 
@@ -250,8 +274,7 @@ def comparison_batch(tri_a: np.ndarray, tri_b: np.ndarray, eps) -> BatchResult:
     """RK/kernels.py:301-401.  Degenerate triangles must be filtered by the caller."""
     A = as_triangles(tri_a)
     B = as_triangles(tri_b)
-    eps = _as_eps(eps, A.shape[0])
-    res, _, _ = _run("comparison", A, B, eps, None)
+    res, _, _ = _run("comparison", A, B, _halo(eps, A.shape[0]), None)
     return res
 
 
@@ -259,8 +282,7 @@ def iterative_batch(tri_a: np.ndarray, tri_b: np.ndarray, params: KernelParams, 
     """RK/kernels.py:447-565."""
     A = as_triangles(tri_a)
     B = as_triangles(tri_b)
-    eps = _as_eps(eps, A.shape[0])
-    res, _, _ = _run("iterative", A, B, eps, params)
+    res, _, _ = _run("iterative", A, B, _halo(eps, A.shape[0]), params)
     return res
 
 
@@ -276,9 +298,13 @@ def hybrid_batch(
     A = as_triangles(tri_a)
     B = as_triangles(tri_b)
     n = A.shape[0]
-    eps = _as_eps(eps, n)
+    eps = _halo(eps, n)
     if isinstance(allow_fallback, np.ndarray):
-        res, stats, rc = _run("hybrid", A, B, eps, params, allow=allow_fallback)
+        # the reference ANDs the mask into the open pairs (RK/kernels.py:590-591):
+        # numpy broadcasting, so a scalar / (1,) mask applies to every pair and
+        # any other shape than (n,) raises ValueError
+        allow = np.broadcast_to(np.asarray(allow_fallback).astype(bool), (n,))
+        res, stats, rc = _run("hybrid", A, B, eps, params, allow=allow)
     elif not allow_fallback:
         res, _, _ = _run("iterative", A, B, eps, params)
         if counters is not None:
@@ -330,8 +356,7 @@ def batch_closest(pairs, params: KernelParams | None = None, counters: KernelCou
     A = as_triangles(np.asarray([p[0] for p in pairs], dtype=REAL))
     B = as_triangles(np.asarray([p[1] for p in pairs], dtype=REAL))
     n = A.shape[0]
-    eps = np.full(n, params.epsilon, dtype=REAL)
-    res, stats, _ = _run("hybrid", A, B, eps, params)
+    res, stats, _ = _run("hybrid", A, B, np.asarray(params.epsilon, dtype=REAL), params)
     if counters is not None:
         counters.iterative_invocations += n
         counters.comparison_invocations += int(stats.comparison)
@@ -352,9 +377,10 @@ def batch_closest(pairs, params: KernelParams | None = None, counters: KernelCou
 
 
 def _pair_max_sq_edge(A: np.ndarray, B: np.ndarray) -> np.ndarray:
+    # 3-term sums through einsum: the reference's reduction order (RK:409-414)
     def longest(T):
         e = np.roll(T, -1, axis=1) - T
-        return (e * e).sum(axis=2).max(axis=1)
+        return np.einsum("ijk,ijk->ij", e, e).max(axis=1)
     return np.maximum(longest(A), longest(B))
 
 
@@ -381,13 +407,17 @@ def _diff(A, B, x):
     return d, (e1a, e2a, e1b, e2b)
 
 
+def _dot(u, v):
+    return np.einsum("ij,ij->i", u, v)
+
+
 def functional_value(t1, t2, a1, b1, a2, b2, params: KernelParams | None = None) -> float:
     params = params or KernelParams()
     A, B = as_triangles(t1), as_triangles(t2)
     x = np.array([[a1, b1, a2, b2]], dtype=REAL)
     d, _ = _diff(A, B, x)
     alpha = params.alpha_iterative * _pair_max_sq_edge(A, B)
-    return 0.5 * float((d * d).sum()) + float(_penalty_value(x, alpha)[0])
+    return 0.5 * float(_dot(d, d)[0]) + float(_penalty_value(x, alpha)[0])
 
 
 def gradient_of_J(t1, t2, a1, b1, a2, b2, params: KernelParams | None = None) -> np.ndarray:
@@ -395,6 +425,6 @@ def gradient_of_J(t1, t2, a1, b1, a2, b2, params: KernelParams | None = None) ->
     A, B = as_triangles(t1), as_triangles(t2)
     x = np.array([[a1, b1, a2, b2]], dtype=REAL)
     d, (e1a, e2a, e1b, e2b) = _diff(A, B, x)
-    grad_hat = np.stack([(d * e1a).sum(1), (d * e2a).sum(1), -(d * e1b).sum(1), -(d * e2b).sum(1)], axis=1)
+    grad_hat = np.stack([_dot(d, e1a), _dot(d, e2a), -_dot(d, e1b), -_dot(d, e2b)], axis=1)
     alpha = params.alpha_iterative * _pair_max_sq_edge(A, B)
     return (grad_hat + _penalty_gradient(x, alpha))[0]

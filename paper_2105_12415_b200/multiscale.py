@@ -130,45 +130,55 @@ class MultiscaleResult:
 
 def multiscale_contacts(forest: Forest, pairs, params, *, strict=True, max_contacts=1 << 20,
                         stream=None) -> MultiscaleResult:
-    """Traverse every (particle_i, particle_j) of ``pairs`` (n, 2) on the device."""
+    """Traverse every (particle_i, particle_j) of ``pairs`` (n, 2) on the device.
+
+    ``max_contacts`` sizes the first attempt's contact list; when the traversal
+    finds more (the count is exact), it is re-run with room for all of them, so
+    the result never depends on which contacts won the atomic slots."""
     import torch
     from .device import _DT, _p
 
     pairs = np.asarray(pairs, np.int64).reshape(-1, 2)
     roots = np.ascontiguousarray(forest.base[pairs].astype(np.int32))
     dev, dt = forest.tris.device, forest.tris.dtype
-    idx = torch.empty((max_contacts, 3), dtype=torch.int32, device=dev)
-    pa = torch.empty((max_contacts, 3), dtype=dt, device=dev)
-    pb = torch.empty((max_contacts, 3), dtype=dt, device=dev)
-    n_contacts = ctypes.c_int64(0)
-    checks = np.zeros(forest.max_height + 1, np.int64)
-    st = _abi.TcStats()
-    st.min_distance = float("inf")
     p = _abi.params_struct(params, _abi.TC_STRICT if strict else 0)
     s = stream if stream is not None else torch.cuda.current_stream(dev)
     fn = getattr(_abi.load(), f"tc_multiscale_{_DT[dt]}")
-    t0 = time.perf_counter()
-    rc = fn(_p(forest.tris), _p(forest.owner), _p(forest.motions), _p(forest.eps), _p(forest.child_off), _p(forest.child_ids), _p(forest.is_fine),
-            _p(forest.height), int(forest.max_height), roots.ctypes.data, int(roots.shape[0]), ctypes.byref(p),
-            int(max_contacts), _p(idx), _p(pa), _p(pb), ctypes.byref(n_contacts), checks.ctypes.data,
-            ctypes.byref(st), ctypes.c_void_p(s.cuda_stream))
-    call_ms = (time.perf_counter() - t0) * 1e3
-    if rc == _abi.TC_EDEGENERATE:
-        from .kernels import DegenerateTriangle
-        raise DegenerateTriangle("degenerate triangle in comparison fallback")
-    _abi.check(rc, "tc_multiscale")
-    n = int(n_contacts.value)
-    m = min(n, max_contacts)
+    cap = max(int(max_contacts), 1)
+    while True:
+        idx = torch.empty((cap, 3), dtype=torch.int32, device=dev)
+        pa = torch.empty((cap, 3), dtype=dt, device=dev)
+        pb = torch.empty((cap, 3), dtype=dt, device=dev)
+        n_contacts = ctypes.c_int64(0)
+        checks = np.zeros(forest.max_height + 1, np.int64)
+        st = _abi.TcStats()
+        st.min_distance = float("inf")
+        t0 = time.perf_counter()
+        rc = fn(_p(forest.tris), _p(forest.owner), _p(forest.motions), _p(forest.eps), _p(forest.child_off),
+                _p(forest.child_ids), _p(forest.is_fine), _p(forest.height), int(forest.max_height),
+                roots.ctypes.data, int(roots.shape[0]), ctypes.byref(p), int(cap), _p(idx), _p(pa), _p(pb),
+                ctypes.byref(n_contacts), checks.ctypes.data, ctypes.byref(st), ctypes.c_void_p(s.cuda_stream))
+        call_ms = (time.perf_counter() - t0) * 1e3
+        if rc == _abi.TC_EDEGENERATE:
+            from .kernels import DegenerateTriangle
+            raise DegenerateTriangle("degenerate triangle in comparison fallback")
+        _abi.check(rc, "tc_multiscale")
+        n = int(n_contacts.value)
+        if n <= cap:
+            break
+        cap = n  # the list overflowed: traverse again with room for every contact
     # order by (pair, id_i, id_j) on the device: three stable sorts, last key first
-    d_idx = idx[:m]
-    perm = torch.arange(m, device=dev)
-    for col in (2, 1, 0):
-        perm = perm[torch.sort(d_idx[perm, col], stable=True).indices]
-    ih = d_idx[perm].cpu().numpy()
+    with torch.cuda.stream(s):
+        d_idx = idx[:n]
+        perm = torch.arange(n, device=dev)
+        for col in (2, 1, 0):
+            perm = perm[torch.sort(d_idx[perm, col], stable=True).indices]
+        ih = d_idx[perm].cpu().numpy()
+        pa_h = pa[:n][perm].cpu().numpy()
+        pb_h = pb[:n][perm].cpu().numpy()
     stats = {k: getattr(st, k) for k in ("iterative", "comparison", "fallback", "degenerate", "contacts",
                                          "intersecting", "min_distance")}
-    return MultiscaleResult(n, ih[:, 0], ih[:, 1], ih[:, 2], pa[:m][perm].cpu().numpy(),
-                            pb[:m][perm].cpu().numpy(), checks, stats, call_ms)
+    return MultiscaleResult(n, ih[:, 0], ih[:, 1], ih[:, 2], pa_h, pb_h, checks, stats, call_ms)
 
 
 def contact_points(forest: Forest, res: MultiscaleResult, pairs):

@@ -140,11 +140,13 @@ def blocks_hybrid(meshes, blocks, params, *, motions=None, block_eps=None, mesh_
     (unordered; ``sort_contacts`` orders them like the reference).
     """
     import torch
-    from .device import _DT, _p
+    from .device import _DT, _on_stream, _p
 
     if meshes.dtype not in _DT or not meshes.is_cuda or not meshes.is_contiguous():
         raise ValueError("meshes must be a contiguous CUDA float64/float32 tensor (N, T, 3, 3)")
-    blocks = blocks.to(device=meshes.device, dtype=torch.int32).contiguous()
+    blocks = torch.as_tensor(blocks).to(device=meshes.device, dtype=torch.int32).contiguous()
+    if blocks.dim() != 2 or blocks.shape[1] != 2:
+        raise ValueError("blocks must be (nb, 2) mesh indices")
     dev, dt = meshes.device, meshes.dtype
     out = {
         "n_contacts": torch.zeros(1, dtype=torch.int64, device=dev),
@@ -161,6 +163,16 @@ def blocks_hybrid(meshes, blocks, params, *, motions=None, block_eps=None, mesh_
         motions = motions.to(device=dev, dtype=dt).contiguous()
     if mesh_tris is not None:
         mesh_tris = torch.as_tensor(mesh_tris, dtype=torch.int32).to(dev).contiguous()
+        if mesh_tris.numel() != meshes.shape[0]:
+            raise ValueError("mesh_tris must hold one count per mesh")
+    if block_eps is not None and block_eps.numel() != blocks.shape[0]:
+        raise ValueError("block_eps must hold one halo per block")
+    if motions is not None and tuple(motions.shape) != (meshes.shape[0], 7):
+        raise ValueError("motions must be (N, 7): quaternion (w, x, y, z) + translation")
+    if stats is not None and (stats.device != dev or stats.dtype != torch.int64 or stats.numel() != 7):
+        raise ValueError("stats must be the 7-word int64 tensor of device.new_stats() on the meshes' device")
+    for t in (blocks, block_eps, motions, mesh_tris, *out.values()):
+        _on_stream(t, st)
     fn = getattr(_abi.load(), f"tc_blocks_hybrid_{_DT[dt]}")
     rc = fn(_p(meshes), int(meshes.shape[1]), int(meshes.shape[0]), _p(mesh_tris), _p(motions), _p(blocks),
             int(blocks.shape[0]),
@@ -172,9 +184,16 @@ def blocks_hybrid(meshes, blocks, params, *, motions=None, block_eps=None, mesh_
 
 
 def sort_contacts(out: dict) -> dict:
-    """Host copy of the contact list ordered by (block, tri_a, tri_b)."""
+    """Host copy of the contact list ordered by (block, tri_a, tri_b).
+
+    Raises if the launch found more contacts than ``max_contacts`` slots:
+    the stored subset would depend on atomic slot order (rerun with
+    ``max_contacts >= n_contacts``; the count is exact)."""
     n = int(out["n_contacts"].item())
-    m = min(n, out["idx"].shape[0])
+    if n > out["idx"].shape[0]:
+        raise RuntimeError(f"{n} contacts found but only max_contacts = {out['idx'].shape[0]} stored; "
+                           "rerun blocks_hybrid with max_contacts >= n_contacts")
+    m = n
     idx = out["idx"][:m].cpu().numpy()
     order = np.lexsort((idx[:, 2], idx[:, 1], idx[:, 0]))
     res = {"n_contacts": n, "idx": idx[order]}

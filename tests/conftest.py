@@ -36,3 +36,9 @@ def oracle_lib():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="session")
+def golden_r2():
+    """Round-2 fixtures from the reference (tests/golden/make_golden_r2.py)."""
+    return {real: dict(np.load(GOLDEN / f"r2_{real}.npz")) for real in DTYPES}

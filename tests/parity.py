@@ -78,15 +78,20 @@ def point_sensitivity(O, fn, A, B, dtype, base, reps=6, seed=1, bary=False):
     return worst
 
 
-def compare_fast(O, variant, A, B, pkw, got, dtype, max_excused=None):
-    """Compare one fast-mode result (dict of numpy columns incl. ids) against the oracle."""
+def compare_fast(O, variant, A, B, pkw, got, dtype, max_excused=None, eps=None, allow=None):
+    """Compare one fast-mode result (dict of numpy columns incl. ids) against the oracle.
+
+    ``eps``: per-pair halos (default: the params' epsilon for every pair);
+    ``allow``: the hybrid's per-pair fallback mask (RK/kernels.py:589-593) --
+    open pairs outside it keep their iterative result."""
     dtype = np.dtype(dtype)
     tau = TAU[dtype]
     A = np.ascontiguousarray(A, dtype)
     B = np.ascontiguousarray(B, dtype)
     n = len(A)
     p = O.make_params(**pkw)
-    eps = np.full(n, p.epsilon, dtype)
+    eps = np.full(n, p.epsilon, dtype) if eps is None else np.ascontiguousarray(eps, dtype)
+    allow = np.ones(n, bool) if allow is None else np.asarray(allow, bool)
     th = O.default_threads()
     cm = O.comparison(A, B, eps, dtype, threads=th)
     it = O.iterative(A, B, p, eps, dtype, threads=th)
@@ -114,12 +119,12 @@ def compare_fast(O, variant, A, B, pkw, got, dtype, max_excused=None):
     else:
         # open pairs fall back unless a triangle is degenerate (then kind 3)
         degen = O.degenerate(A, dtype, threads=th) | O.degenerate(B, dtype, threads=th)
-        fb_ref = (it["kind"] == 2) & ~degen
+        fb_ref = (it["kind"] == 2) & allow & ~degen
     path_ok = (fb_got == fb_ref) | t_settle
     # the oracle result of the path the GPU took
     ref = {k: np.where(fb_got.reshape((-1,) + (1,) * (cm[k].ndim - 1)), cm[k], it[k]) for k in cm}
     if variant == "hybrid":
-        ref["kind"] = np.where((it["kind"] == 2) & degen & ~fb_got, np.int8(3), ref["kind"])
+        ref["kind"] = np.where((it["kind"] == 2) & allow & degen & ~fb_got, np.int8(3), ref["kind"])
 
     # discrete checks on the GPU's path
     cmp_rows = fb_got

@@ -43,7 +43,7 @@ def test_ctypes_binding_covers_header(lib_path):
     from paper_2105_12415_b200 import _abi
     assert set(header_symbols()) == set(_abi.SIGNATURES)
     lib = _abi.load(lib_path)
-    assert lib.tc_abi_version() == 1
+    assert lib.tc_abi_version() == _abi.TC_ABI_VERSION == 2
     p = _abi.TcParams()
     lib.tc_params_default(ctypes.byref(p))
     assert (p.epsilon, p.n_iterative, p.alpha_iterative, p.move_factor) == (1e-2, 4, 10.0, 0.25)

@@ -55,6 +55,29 @@ def test_gradient_matches_finite_differences():
         assert np.linalg.norm(g - fd) / max(np.linalg.norm(fd), 1e-12) < 1e-5
 
 
+def test_gradient_and_functional_equal_reference(golden_r2):
+    """RK/kernels.py:677-717 at acceptance criterion 2's points (seed 20260802):
+    bit-identical to the reference's own values (tests/golden/make_golden_r2.py)."""
+    ref = golden_r2["float64"]
+    p = K.KernelParams()
+    for row, g, v in zip(ref["grad_points"], ref["grad_gradient"], ref["grad_value"]):
+        A, B, x = row[:9].reshape(3, 3), row[9:18].reshape(3, 3), row[18:]
+        assert np.array_equal(K.gradient_of_J(A, B, *x, p), g)
+        assert K.functional_value(A, B, *x, p) == v
+
+
+def test_allow_mask_shapes_follow_numpy_broadcasting():
+    """RK/kernels.py:590-591 ANDs the mask into the open pairs: a mask that
+    does not broadcast to (n,) raises ValueError before any device work."""
+    A = np.zeros((4, 3, 3))
+    with pytest.raises(ValueError):
+        K.hybrid_batch(A, A, K.KernelParams(), None, 1e-2, allow_fallback=np.ones(3, bool))
+    with pytest.raises(ValueError):
+        K.hybrid_batch(A, A, K.KernelParams(), None, 1e-2, allow_fallback=np.ones((2, 4), bool))
+    with pytest.raises(ValueError):
+        K.hybrid_batch(A, A, K.KernelParams(), None, np.ones(3))
+
+
 # ---- GPU: the drop-in computes through the C ABI ----------------------------
 
 torch = pytest.importorskip("torch")
@@ -123,9 +146,20 @@ class TestKnownAnswers:
         p = K.KernelParams()
         bad = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float)
         good = off(U, dz=1.0)
-        out = K.batch_closest([(U, good), (bad, off(U, dx=40.0, dz=0.01)), (U, good)], p)
+        # the collinear triangle against this one stays NOT_TERMINATED after the
+        # default 4 sweeps (oracle-checked), so it reaches the fallback, whose
+        # degenerate screen reports it positionally (RK/kernels.py:654-668)
+        open_b = np.array([[0.206, 0.02, 0.383], [-0.516, -0.114, -0.337], [0.419, 0.028, -0.205]])
+        assert K.closest_iterative(bad, open_b, p).kind == K.Kind.NOT_TERMINATED
+        c = K.KernelCounters()
+        out = K.batch_closest([(U, good), (bad, open_b), (U, good), (bad, good)], p, c)
         assert isinstance(out[0], K.DistanceResult) and isinstance(out[2], K.DistanceResult)
+        assert isinstance(out[1], K.DegenerateTriangle) and "pair 1" in str(out[1])
+        assert isinstance(out[3], K.DistanceResult)  # settled: the degenerate triangle never reaches the fallback
         assert out[0].distance == pytest.approx(1.0, abs=1e-9)
+        assert (c.iterative_invocations, c.fallback_invocations) == (4, 0)
+        with pytest.raises(K.DegenerateTriangle):
+            K.closest_hybrid(bad, open_b, p)
 
     def test_batch_closest_equals_scalar_map(self):
         rng = np.random.default_rng(8)

@@ -144,15 +144,17 @@ def test_degenerate_fallback_marks_pairs():
     """RK/kernels.py:598-600: degenerate triangles only matter on fallback."""
     U = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float)
     bad = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float)
-    crawler = U + [40.0, 0, 0.01]
+    # NOT_TERMINATED after the default 4 sweeps against `bad` (oracle-checked
+    # below), so this pair reaches the fallback and its screen
+    open_b = np.array([[0.206, 0.02, 0.383], [-0.516, -0.114, -0.337], [0.419, 0.028, -0.205]])
     far = U + [0, 0, 1.0]
     A = np.stack([bad, bad, U])
-    B = np.stack([far, crawler, far])
+    B = np.stack([far, open_b, far])
     hy, st = run_dev("hybrid", A, B, "float64", "def", True)
-    assert hy["kind"][0] != 2                     # settled: never consults the comparison kernel
+    assert hy["kind"][0] == 0                     # settled: never consults the comparison kernel
     assert hy["kind"][2] == 0
-    if hy["kind"][1] == 3:
-        assert st["degenerate"] == 1
+    assert hy["kind"][1] == 3 and st["degenerate"] == 1 and st["fallback"] == 0
+    assert (hy["ids"][1, 3] & 8) > 0
     assert not (hy["kind"] == 2).any()
 
 

@@ -87,3 +87,28 @@ def test_oracle_threads_invariant(oracle_lib, golden_inputs):
     for k in h1:
         assert np.array_equal(h1[k], h8[k])
     assert np.array_equal(c1, c8)
+
+
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_oracle_degenerate_rel_tol(oracle_lib, golden_inputs, golden_r2, real):
+    """degenerate_mask(T, rel_tol) at non-default tolerances (RK/geometry.py:68-75)."""
+    ref = golden_r2[real]
+    for i, tol in enumerate(ref["degtol_rel_tols"]):
+        m = oracle_lib.degenerate(golden_inputs["degenerate_T"], DTYPES[real], rel_tol=float(tol))
+        assert np.array_equal(m, ref[f"degtol_{i}"]), tol
+
+
+def test_oracle_acceptance_criterion_1(oracle_lib, golden_r2):
+    """The 10,000 scene-drawn pairs of RT/test_acceptance.py:69-87: the oracle's
+    comparison (incl. ids) and hybrid are bit-identical to the reference's."""
+    O = oracle_lib
+    ref = golden_r2["float64"]
+    A, B = ref["crit1_A"], ref["crit1_B"]
+    p = O.make_params()
+    eps = np.full(len(A), p.epsilon)
+    cm = O.comparison(A, B, eps, threads=O.default_threads())
+    _assert_cols(ref, "crit1_comparison", cm)
+    assert np.array_equal(ref["crit1_comparison_ids"], cm["ids"])
+    hy, counts, rc = O.hybrid(A, B, p, eps, threads=O.default_threads())
+    assert rc == 0
+    _assert_cols(ref, "crit1_hybrid", hy)
