@@ -2,24 +2,37 @@
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Workload (config 1 of BASELINE.json): 16,777,216 = 2^24 random triangle
-pairs per GPU from the chunked cfg0 generator (seed 0, separation
-U[-0.1, 0.5]), fp64, planar SoA layout [18][n] resident in HBM, hybrid
-kernel at (16 sweeps, eps 1e-6), full result record written.  A step is one
-pass of the hot path over the batch: stats reset, the hybrid kernel, and
-(N > 1) the NCCL all-reduce of the stats record.  Rank r of N works on
-pairs [r*2^24, (r+1)*2^24) of the same generator (weak scaling).  Inputs
-(2.4 GB) and outputs (1.5 GB) exceed the 126 MB L2, so no flush is needed.
+``--gpus N`` without a torchrun environment relaunches itself as N ranks
+(``torch.distributed.run``, one process per GPU, NCCL); under torchrun the
+ranks come from RANK / LOCAL_RANK / WORLD_SIZE.
+
+Headline workload (config 1 of BASELINE.json): 16,777,216 = 2^24 random
+triangle pairs per GPU from the chunked cfg0 generator (seed 0, separation
+U[-0.1, 0.5]), fp64, planar SoA layout [18][n] resident in HBM, hybrid kernel
+at (16 sweeps, eps 1e-6), full result record written.  A step is one pass of
+the hot path over the batch: stats reset, the hybrid kernel, and (N > 1) the
+all-reduce of the stats record.  Rank r of N works on pairs [r*2^24,
+(r+1)*2^24) of the same generator (weak scaling).  Inputs (2.4 GB) and
+outputs (1.5 GB) exceed the 126 MB L2, so no flush is needed.
+
+Every line also carries ``configs.cfg4_strong``: BASELINE.json config 4,
+2^28 pairs IN TOTAL (separation U[-0.05, 0.2]) sharded over the N ranks by
+contiguous ranges, reduce-only (tc_stats), with the all-reduce of the
+counters and minimum distance -- strong scaling at every N.  Its inputs come
+from the device Philox generator of the same distribution
+(tc_random_pairs_soa_f64: host numpy would take minutes for 2^28 pairs).
 
 ``e2e`` times the same workload through the reference-facing C-ABI host
-entry point tc_run_host_f64 (the call the drop-in ``tricontact.kernels``
-makes) with pinned host buffers in the reference's (n,3,3) layout: H2D of
-the inputs, kernel and D2H of the full result record are inside its timed
-region.
+entry point tc_run_host_f64 with pinned host buffers in the reference's
+(n,3,3) layout; ``e2e_dropin`` through the drop-in module itself
+(``kernels.hybrid_batch`` on plain pageable numpy arrays, strict and fast):
+H2D of the inputs, kernel and D2H of the full result record are inside the
+timed region.
 
 ``--impl reference`` times the reference's CPU path -- the oracle port
 (oracle/tc_oracle.c: the reference is pure numpy and cannot travel to the
-GPU box) -- with every host thread, on bounded samples of the same workload.
+GPU box) -- with every host thread, on the same cfg1 workload: each step is a
+slice of the 2^24 pairs, the slices cycling through all of them.
 """
 
 from __future__ import annotations
@@ -144,8 +157,22 @@ def cpu_oracle_rate(seconds: float, chunk: int, threads: int, start: int = 0):
     return done / elapsed, done
 
 
-def run_reference(args, rank):
-    """--impl reference: the CPU path on the host cores, rank 0 only."""
+def cfg1_config(n, world, strict):
+    """The workload dict both arms print (GPU and reference)."""
+    return {"workload": "cfg1: 2^24 random triangle pairs per GPU, hybrid fp64, 16 sweeps, eps 1e-6",
+            "pairs_per_gpu": n, "layout": "SoA [18][n] in HBM", "rounding": "strict" if strict else "fast",
+            "l2": "inputs 2.4 GB + outputs 1.5 GB per GPU > 126 MB L2 (no flush needed)",
+            "parallelism": f"dp{world} contiguous shards + one all-gather of the stats record" if world > 1
+            else "1 GPU"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU path on the host cores, rank 0 only.
+
+    Same workload as the GPU arm (cfg1: the 2^24 pairs of the chunked
+    generator, hybrid (16, 1e-6)); each timed step is a distinct slice of them,
+    max(2^24 / K, 2^20) pairs, cycling through the whole set, so K steps cover
+    at least 16M distinct pairs in a few seconds of CPU time."""
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
@@ -153,31 +180,57 @@ def run_reference(args, rank):
     import oracle
     from paper_2105_12415_b200 import workloads as W
     oracle.build()
-    sample = 1 << 16
+    n_all = args.n
+    sample = min(n_all, max(-(-n_all // max(args.steps, 1)), 1 << 20))
     p = oracle.make_params(**PARAMS)
-    A, B = W.random_pairs(sample, seed=0, sep=SEP)
-    for _ in range(args.warmup):
-        oracle.hybrid(A, B, p, PARAMS["epsilon"], threads=threads)
-    t0 = time.perf_counter()
+    A, B = W.random_pairs_mp(n_all, seed=0, sep=SEP)
+    for k in range(args.warmup):
+        oracle.hybrid(A[: 1 << 16], B[: 1 << 16], p, PARAMS["epsilon"], threads=threads)
+    elapsed, done, off = 0.0, 0, 0
     for _ in range(args.steps):
-        _, _, rc = oracle.hybrid(A, B, p, PARAMS["epsilon"], threads=threads)
+        lo = off % n_all
+        hi = min(lo + sample, n_all)
+        a, b = A[lo:hi], B[lo:hi]
+        t0 = time.perf_counter()
+        _, _, rc = oracle.hybrid(a, b, p, PARAMS["epsilon"], threads=threads)
+        elapsed += time.perf_counter() - t0
         assert rc == 0
-    dt = time.perf_counter() - t0
-    value = sample * args.steps / dt
+        done += hi - lo
+        off = hi
+    value = done / elapsed
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded cfg0 generator)",
-        "config": {"workload": "cfg1: hybrid fp64, 16 sweeps, eps 1e-6, random pairs sep U[-0.1,0.5]",
-                   "pairs_per_step": sample, "layout": "(n,3,3) host"},
+        "data": "synthetic (seeded cfg0/cfg1 generator, SURVEY.md 8d)",
+        "config": cfg1_config(n_all, world, False),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} pairs of the cfg1 generator per step (oracle/tc_oracle.c, "
-                                   "C restatement of RK/kernels.py, bit-identical to the reference)",
+                         "sample": f"{done} pairs of the 2^24 cfg1 set in {args.steps} steps of {sample} distinct "
+                                   f"pairs (slices cycling through the set), hybrid (16, 1e-6), oracle/tc_oracle.c "
+                                   "(C restatement of RK/kernels.py, bit-identical to the reference) on every host "
+                                   "thread; generation excluded",
                          "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N outside torchrun: relaunch this command as N ranks."""
+    import socket
+    if args.impl != "reference" and not args.share_gpu:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but only {have} CUDA devices"}), flush=True)
+            return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------------------
@@ -187,20 +240,25 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_PAIRS, help="pairs per GPU")
+    ap.add_argument("--n", type=int, default=N_PAIRS, help="pairs per GPU (cfg1)")
+    ap.add_argument("--cfg4-n", type=int, default=CFG4_PAIRS, help="pairs in total (cfg4 strong scaling)")
     ap.add_argument("--strict", action="store_true", help="time the bit-exact TC_STRICT build")
-    ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu baseline / variant table")
-    ap.add_argument("--config", default="cfg1", choices=["cfg1", "cfg4"],
-                    help="cfg1: 2^24 pairs per GPU, full record (weak scaling, default); "
-                         "cfg4: 2^28 pairs in total sharded over the GPUs, reduce-only (strong scaling)")
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu baseline / variant table / configs")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the cfg4 strong-scaling run")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: tests of the multi-rank path on one GPU)")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="tests only: every rank on cuda:0 (functional check of the N-rank path, not a measurement)")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.share_gpu else int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        return run_reference(args, rank)
+        return run_reference(args, rank, world)
 
     import torch
     import torch.distributed as dist
@@ -209,33 +267,27 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     lib = _abi.load()
-    cfg4 = args.config == "cfg4"
-    if cfg4:
-        n_total = args.n if args.n != N_PAIRS else CFG4_PAIRS
-        start, n = shard.shard_range(n_total, rank, world)
-        sep = CFG4_SEP
-    else:
-        n, start, sep = args.n, rank * args.n, SEP
+    n, start, sep = args.n, rank * args.n, SEP
 
     # ---- inputs: this rank's range of the chunked generator, SoA planes in HBM
     # (generated on all host cores in slices, uploaded slice by slice)
     planes = torch.empty((18, n), dtype=torch.float64, device=dev)
-    A = B = None
+    A = np.empty((n, 3, 3))
+    B = np.empty((n, 3, 3))
     slice_n = 1 << 23
     for lo in range(0, n, slice_n):
         hi = min(n, lo + slice_n)
         a, b = W.random_pairs_mp(hi - lo, seed=0, sep=sep, start=start + lo)
         planes[:, lo:hi] = torch.from_numpy(W.to_soa(a, b)).to(dev)
-        if not cfg4:
-            if A is None:
-                A = np.empty((n, 3, 3))
-                B = np.empty((n, 3, 3))
-            A[lo:hi] = a
-            B[lo:hi] = b
+        A[lo:hi] = a
+        B[lo:hi] = b
     ta, tb = planes[:9], planes[9:]
-    out = {} if cfg4 else D.alloc_outputs(n, torch.float64, dev, soa=True)
+    out = D.alloc_outputs(n, torch.float64, dev, soa=True)
     stats = D.new_stats(dev)
     params = D.Params(**PARAMS)
     stream = torch.cuda.current_stream(dev)
@@ -272,40 +324,25 @@ def main():
     launches = D.launch_count() - launches0
     ms_total = t_start.elapsed_time(t_end)
     ms_kernel = sum(a.elapsed_time(b) for a, b in kev) / args.steps
-    t = torch.tensor([ms_total, ms_kernel], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total, ms_kernel = float(t[0]), float(t[1])
+    ms_total, ms_kernel = max_over_ranks(torch, dist, world, dev, ms_total, ms_kernel)
     ms_step = ms_total / args.steps
     st = shard.stats_dict(stats)  # after the last step's all-reduce: whole-job tallies
-    n_job = n_total if cfg4 else n * world
+    n_job = n * world
     value = n_job / (ms_step / 1e3)
 
     # ---- roofline of the dominant kernel (hybrid_kernel): FP64 pipe
-    n_local = n
-    fb_local = st["fallback"] * n_local / n_job
-    fbx_local = st["intersecting"] * n_local / n_job
+    fb_local = st["fallback"] / world
+    fbx_local = st["intersecting"] / world
     # achieved = the algorithmic work SURVEY.md 8(d) defines per pair (App. A),
     # x the pairs of one launch, / the launch's duration; the work this kernel
     # actually executes (intersecting fallbacks skip the feature tests) is
     # reported beside it
-    flops = flops_reference_model(n_local, PARAMS["n_iterative"], fb_local, fbx_local)
-    flops_exec = flops_executed(n_local, PARAMS["n_iterative"], fb_local, fbx_local)
+    flops = flops_reference_model(n, PARAMS["n_iterative"], fb_local, fbx_local)
+    flops_exec = flops_executed(n, PARAMS["n_iterative"], fb_local, fbx_local)
     achieved_tf = flops / (ms_kernel / 1e3) / 1e12
-    sink = torch.empty(4096, dtype=torch.float64, device=dev)
-    blocks = 148 * 8
-    lib.tc_fma_probe(1, blocks, 64, ctypes.c_void_p(sink.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    best = 0.0
-    for _ in range(5):
-        e0.record(stream)
-        fl = lib.tc_fma_probe(1, blocks, 2048, ctypes.c_void_p(sink.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
-        e1.record(stream)
-        torch.cuda.synchronize()
-        best = max(best, fl / (e0.elapsed_time(e1) / 1e3) / 1e12)
-    peak_tf = best
-    bytes_per_pair = 144 if cfg4 else 144 + 89  # SoA inputs (+ full result record unless reduce-only)
-    hbm_gbs = n_local * bytes_per_pair / (ms_kernel / 1e3) / 1e9
+    peak_tf = fma_peak(torch, lib, stream, dev, fp64=True)
+    bytes_per_pair = 144 + 89  # SoA inputs + full result record
+    hbm_gbs = n * bytes_per_pair / (ms_kernel / 1e3) / 1e9
     peaks = {}
     try:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -318,7 +355,7 @@ def main():
     if prof.exists():
         try:
             pj = json.loads(prof.read_text())
-            if pj.get("n") == n_local and not cfg4:
+            if pj.get("n") == n:
                 traffic = pj.get("dram_bytes_per_launch")
                 traffic_note = pj.get("source")
         except ValueError:
@@ -326,8 +363,8 @@ def main():
     roofline = {
         "bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
         "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
-        "traffic_source": traffic_note, "algorithmic_bytes_per_launch": n_local * bytes_per_pair,
-        "kernel": "hybrid_kernel<double,fast,soa>", "kernel_ms": ms_kernel,
+        "traffic_source": traffic_note, "algorithmic_bytes_per_launch": n * bytes_per_pair,
+        "kernel": f"hybrid_kernel<double,{'strict' if args.strict else 'fast'},soa>", "kernel_ms": ms_kernel,
         "flops_per_launch": flops,
         "flop_model": "SURVEY.md 8(d)/App. A algorithmic work: n(200+88N) + 1199 fallback + 254 fallback&intersect "
                       "(N = 16 sweeps; fallback and intersect counts from this run's tc_stats)",
@@ -338,38 +375,28 @@ def main():
         "hbm": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_gbs / hbm_peak,
                 "bytes_per_pair": bytes_per_pair, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
     }
-
-    if cfg4:
-        cfg = {"workload": "cfg4: 2^28 random triangle pairs in total, sep U[-0.05,0.2], hybrid fp64, 16 sweeps, "
-                           "eps 1e-6, reduce-only (tc_stats), contiguous shards",
-               "pairs_total": n_total, "pairs_per_gpu": n, "layout": "SoA [18][n] in HBM",
-               "rounding": "strict" if args.strict else "fast",
-               "l2": f"inputs {n * 144 / 1e9:.1f} GB per GPU > 126 MB L2 (no flush needed)",
-               "parallelism": f"dp{world} contiguous shards + NCCL all-reduce of stats" if world > 1 else "1 GPU"}
-    else:
-        cfg = {"workload": "cfg1: 2^24 random triangle pairs per GPU, hybrid fp64, 16 sweeps, eps 1e-6",
-               "pairs_per_gpu": n, "layout": "SoA [18][n] in HBM", "rounding": "strict" if args.strict else "fast",
-               "l2": "inputs 2.4 GB + outputs 1.5 GB per GPU > 126 MB L2 (no flush needed)",
-               "parallelism": f"dp{world} contiguous shards + NCCL all-reduce of stats" if world > 1 else "1 GPU"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if cfg4 else "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded cfg0/cfg1 generator, SURVEY.md 8d)",
-        "config": cfg,
+        "config": cfg1_config(n, world, args.strict),
         "roofline": roofline,
         "gpu_launches": launches,
         "stats": st,
         "fallback_rate": st["fallback"] / n_job,
     }
+    line["clocks"] = clk.summary()
+    if args.share_gpu:
+        line["note"] = "--share-gpu: every rank on cuda:0 (functional test of the N-rank path, not a measurement)"
+    configs = {}
+    if not args.no_cfg4:
+        configs["cfg4_strong"] = cfg4_strong(args, torch, dist, D, shard, lib, world, rank, dev, stream, peak_tf)
 
-    clocks = clk.summary()
-    line["clocks"] = clocks
-
-    if not args.no_extras and not cfg4:
-        # ---- e2e through the host C-ABI entry point (pinned host buffers)
+    if not args.no_extras:
+        # ---- e2e through the host C-ABI entry point (pinned host buffers), every rank
         line["e2e"] = e2e_measure(lib, _abi, torch, A, B, n, world, dist, dev)
         if rank == 0 and world == 1:
+            line["e2e_dropin"] = e2e_dropin(A, B)
             threads = len(os.sched_getaffinity(0))
             rate, done = cpu_oracle_rate(10.0, 1 << 17, threads)
             rate1, done1 = cpu_oracle_rate(3.0, 1 << 14, 1)
@@ -379,12 +406,134 @@ def main():
                                               "excluded",
                                     "one_core": {"value": rate1, "sample": f"{done1} pairs, 1 thread"},
                                     "cpu_model": cpu_model()}
-            line["variants"] = variant_table(D, torch, A[: 1 << 22], B[: 1 << 22], dev)
-            line["configs"] = configs_table(D, torch, dev)
+            line["variants"] = variant_table(D, torch, ta, tb, n, dev)
+            line["roofline_f32"] = roofline_f32(D, torch, lib, ta, tb, n, dev, stream)
+            configs.update(configs_table(D, torch, dev))
+    if configs:
+        line["configs"] = configs
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def max_over_ranks(torch, dist, world, dev, *vals):
+    t = torch.tensor(list(vals), dtype=torch.float64, device=dev)
+    if world > 1:
+        if dist.get_backend() == "nccl":
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX)
+            t = h
+    return [float(x) for x in t]
+
+
+def fma_peak(torch, lib, stream, dev, fp64=True):
+    """FP64 (DFMA) or FP32 (FFMA) pipe peak of this GPU, TFLOP/s (tc_fma_probe)."""
+    sink = torch.empty(8192, dtype=torch.float64, device=dev)
+    blocks = 148 * 8
+    s = ctypes.c_void_p(stream.cuda_stream)
+    iters = 2048 if fp64 else 4096
+    lib.tc_fma_probe(1 if fp64 else 0, blocks, 64, ctypes.c_void_p(sink.data_ptr()), s)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(5):
+        e0.record(stream)
+        fl = lib.tc_fma_probe(1 if fp64 else 0, blocks, iters, ctypes.c_void_p(sink.data_ptr()), s)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        best = max(best, fl / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    return best
+
+
+def cfg4_strong(args, torch, dist, D, shard, lib, world, rank, dev, stream, peak_tf, steps=5, warmup=2):
+    """BASELINE.json config 4: 2^28 pairs in total, contiguous shards over the
+    ranks, reduce-only hybrid + all-reduce of the stats record.  Inputs from
+    the device Philox generator of the cfg0 distribution, sep U[-0.05, 0.2]."""
+    n_total = args.cfg4_n
+    start, n = shard.shard_range(n_total, rank, world)
+    planes = torch.empty((18, max(n, 1)), dtype=torch.float64, device=dev)
+    from paper_2105_12415_b200 import _abi
+    _abi.check(lib.tc_random_pairs_soa_f64(4, start, n, CFG4_SEP[0], CFG4_SEP[1],
+                                           ctypes.c_void_p(planes.data_ptr()), ctypes.c_void_p(stream.cuda_stream)),
+               "tc_random_pairs_soa_f64")
+    ta, tb = planes[:9], planes[9:]
+    stats = D.new_stats(dev)
+    params = D.Params(**PARAMS)
+
+    def step(ev=None):
+        D.reset_stats(stats)
+        if ev is not None:
+            ev[0].record(stream)
+        D.run("hybrid", ta, tb, params, soa=True, strict=args.strict, out={}, stats=stats, n=n)
+        if ev is not None:
+            ev[1].record(stream)
+        if world > 1:
+            shard.allreduce_stats(stats)
+
+    for _ in range(warmup):
+        step()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(steps):
+        step(kev[k])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    ms_kernel = sum(a.elapsed_time(b) for a, b in kev) / steps
+    ms_total, ms_kernel, ms_kernel_min = max_over_ranks(torch, dist, world, dev, ms_total, ms_kernel, -ms_kernel)
+    st = shard.stats_dict(stats)
+    ms_step = ms_total / steps
+    fl = flops_reference_model(n_total / world, PARAMS["n_iterative"], st["fallback"] / world,
+                               st["intersecting"] / world)
+    del planes
+    torch.cuda.empty_cache()
+    return {"pairs_total": n_total, "pairs_per_gpu": n_total // world, "n_gpus": world, "steps": steps,
+            "warmup": warmup, "value": n_total / (ms_step / 1e3), "unit": UNIT, "ms_per_step": ms_step,
+            "kernel_ms_max_rank": ms_kernel, "kernel_ms_min_rank": -ms_kernel_min, "scaling": "strong",
+            "fp64_frac": fl / (ms_kernel / 1e3) / 1e12 / peak_tf,
+            "fallback_rate": st["fallback"] / n_total, "stats": st,
+            "workload": "cfg4: 2^28 random pairs in total (cfg0 distribution, sep U[-0.05,0.2], device Philox "
+                        "generator seed 4), hybrid fp64 (16, 1e-6), reduce-only, contiguous shards + all-gather "
+                        "of the stats record",
+            "timing": "CUDA events on the launching stream, max over ranks"}
+
+
+def e2e_dropin(A, B, reps=3):
+    """End to end through the drop-in module: kernels.hybrid_batch on plain
+    pageable numpy arrays (the reference's callers' usage, RK/stepping.py:299,
+    RK/contact.py:131), strict (its default) and fast."""
+    from paper_2105_12415_b200 import kernels as K
+    n = A.shape[0]
+    p = K.KernelParams(**PARAMS)
+    res = {"n": n, "unit": UNIT, "h2d_bytes_per_step": n * 144, "d2h_bytes_per_step": n * 89,
+           "path": "paper_2105_12415_b200.kernels.hybrid_batch(A, B, params, counters, eps) on pageable numpy "
+                   "(n,3,3) arrays -> tc_run_host_f64: pinned staging by the library's copy threads, 3-stream "
+                   "pipeline"}
+    prev = K.rounding()
+    try:
+        for mode in ("strict", "fast"):
+            K.set_rounding(mode)
+            K.hybrid_batch(A[: 1 << 20], B[: 1 << 20], p, None, PARAMS["epsilon"])
+            times = []
+            for _ in range(reps):
+                c = K.KernelCounters()
+                t0 = time.perf_counter()
+                r = K.hybrid_batch(A, B, p, c, PARAMS["epsilon"])
+                times.append(time.perf_counter() - t0)
+                del r
+            sec = statistics.median(times)
+            res[mode] = {"value": n / sec, "ms_per_step": 1e3 * sec, "fallback": c.fallback_invocations}
+    finally:
+        K.set_rounding(prev)
+    return res
 
 
 def e2e_measure(lib, _abi, torch, A, B, n, world, dist, dev, reps=3):
@@ -416,10 +565,7 @@ def e2e_measure(lib, _abi, torch, A, B, n, world, dist, dev, reps=3):
         t0 = time.perf_counter()
         call()
         times.append(time.perf_counter() - t0)
-    t = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    sec = float(t[0])
+    sec, = max_over_ranks(torch, dist, world, dev, statistics.median(times))
     link = pcie_probe(torch, dev)
     # the transfers are the floor: while both directions run each gets the
     # duplex rate, then the larger direction finishes alone at its own rate
@@ -587,29 +733,56 @@ def multiscale_table(D, torch, dev, n_pairs=1024):
     return res
 
 
-def variant_table(D, torch, A, B, dev, reps=3):
-    """Kernel-only rates of every variant x dtype x rounding on 2^22 pairs (SoA, full record)."""
-    from paper_2105_12415_b200 import workloads as W
+def variant_table(D, torch, ta, tb, n, dev, reps=3):
+    """Kernel-only rates of every variant x dtype x rounding on the cfg1 batch
+    (2^24 pairs, SoA in HBM, full record)."""
     res = {}
-    n = A.shape[0]
     P = D.Params(**PARAMS)
     for dt, name in ((torch.float64, "f64"), (torch.float32, "f32")):
-        planes = torch.from_numpy(W.to_soa(A, B)).to(dev, dt)
-        ta, tb = planes[:9], planes[9:]
+        a, b = ta.to(dt), tb.to(dt)
         out = D.alloc_outputs(n, dt, dev, soa=True)
         for variant in ("iterative", "comparison", "hybrid"):
             for strict in (False, True):
-                D.run(variant, ta, tb, P, soa=True, strict=strict, out=out, n=n)
+                D.run(variant, a, b, P, soa=True, strict=strict, out=out, n=n)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 for _ in range(reps):
-                    D.run(variant, ta, tb, P, soa=True, strict=strict, out=out, n=n)
+                    D.run(variant, a, b, P, soa=True, strict=strict, out=out, n=n)
                 e1.record()
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / reps
                 res[f"{variant}_{name}_{'strict' if strict else 'fast'}"] = round(n / (ms / 1e3), 1)
-    res["unit"] = "pairs/s, 2^22 pairs, SoA, full record, (16, 1e-6)"
+        del a, b, out
+    res["unit"] = f"pairs/s, {n} pairs (cfg1), SoA, full record, (16, 1e-6)"
     return res
+
+
+def roofline_f32(D, torch, lib, ta, tb, n, dev, stream, reps=5):
+    """FP32 roofline of hybrid_kernel<float,fast,soa> on the cfg1 batch cast to
+    fp32: SURVEY.md 8(d)'s algorithmic flops (this run's fallback counts) per
+    launch over the launch time, against the in-run FFMA peak."""
+    a, b = ta.to(torch.float32), tb.to(torch.float32)
+    out = D.alloc_outputs(n, torch.float32, dev, soa=True)
+    st = D.new_stats(dev)
+    P = D.Params(**PARAMS)
+    D.run("hybrid", a, b, P, soa=True, out=out, n=n)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for e0, e1 in ev:
+        D.reset_stats(st)
+        e0.record(stream)
+        D.run("hybrid", a, b, P, soa=True, out=out, stats=st, n=n)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = sorted(e0.elapsed_time(e1) for e0, e1 in ev)[reps // 2]
+    s = D.read_stats(st)
+    flops = flops_reference_model(n, PARAMS["n_iterative"], s["fallback"], s["intersecting"])
+    peak = fma_peak(torch, lib, stream, dev, fp64=False)
+    achieved = flops / (ms / 1e3) / 1e12
+    return {"bound": "fp32", "kernel": "hybrid_kernel<float,fast,soa>", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak, "kernel_ms": ms, "pairs_per_s": n / (ms / 1e3),
+            "fallback_rate": s["fallback"] / n, "flops_per_launch": flops,
+            "flop_model": "SURVEY.md 8(d)/App. A, as roofline", "peak_source": "in-run FFMA probe (tc_fma_probe)",
+            "hbm": {"achieved": n * (72 + 45) / (ms / 1e3) / 1e9, "unit": "GB/s", "bytes_per_pair": 72 + 45}}
 
 
 if __name__ == "__main__":

@@ -254,6 +254,15 @@ int tc_degenerate_mask_host_f32(const float* tris, int64_t n, double rel_tol, ui
  * elements. */
 int64_t tc_fma_probe(int fp64, int64_t blocks, int iters, void* sink, void* stream);
 
+/* Benchmark / test workload: pairs [start, start + n) of the cfg0 distribution
+ * (BASELINE.json: A ~ U[0,1]^9; B = A rotated about its centroid by a uniform
+ * random rotation and shifted by s * (random unit vector), s ~ U[sep_lo,
+ * sep_hi]) from a counter-based Philox4x32-10 stream keyed by (seed, pair
+ * index), written as SoA planes [18][n] (device pointer): any shard is
+ * generated independently.  Not numpy's stream: a device generator of the same
+ * distribution (numpy mirror: workloads.philox_pairs). */
+int tc_random_pairs_soa_f64(uint64_t seed, int64_t start, int64_t n, double sep_lo, double sep_hi,
+                            double* planes, void* stream);
 /* Number of kernel launches this library has enqueued since load. */
 int64_t tc_launch_count(void);
 

@@ -1079,6 +1079,78 @@ __global__ void __launch_bounds__(BLOCK) fma_probe_kernel(T* sink, int iters) {
     if (s == T(-1)) sink[blockIdx.x] = s;  // never true; keeps the chains alive
 }
 
+// ---- device workload generator (benchmark / test helper) -------------------------
+// The cfg0 distribution of BASELINE.json (A ~ U[0,1]^9; B = R(q)(A - c_A) + c_A
+// + s u with q ~ N(0,1)^4 and u ~ N(0,1)^3 normalised, s ~ U[lo, hi]) drawn
+// from a counter-based Philox4x32-10 stream keyed by (seed, pair index), so
+// any pair range (a shard) is generated independently, in place, in HBM --
+// the 2^28-pair cfg4 set costs milliseconds instead of minutes of host numpy.
+// workloads.philox_pairs is the numpy mirror (tests/test_workloads.py).
+struct Philox {
+    uint32_t c[4];
+};
+__device__ __forceinline__ Philox philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                                uint32_t k1) {
+    Philox r{{c0, c1, c2, c3}};
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint32_t lo0 = 0xD2511F53u * r.c[0], hi0 = __umulhi(0xD2511F53u, r.c[0]);
+        const uint32_t lo1 = 0xCD9E8D57u * r.c[2], hi1 = __umulhi(0xCD9E8D57u, r.c[2]);
+        r = Philox{{hi1 ^ r.c[1] ^ k0, lo1, hi0 ^ r.c[3] ^ k1, lo0}};
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return r;
+}
+// 53-bit uniform in [0, 1) from two words (numpy's random_standard_uniform recipe)
+__device__ __forceinline__ double u53(uint32_t a, uint32_t b) {
+    return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) * (1.0 / 9007199254740992.0);
+}
+
+__global__ void random_pairs_kernel(uint64_t seed, int64_t start, int64_t n, double lo, double hi, double* planes) {
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32) ^ 0x5EEDu;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t id = (uint64_t)(start + i);
+        double u[18];
+#pragma unroll
+        for (int call = 0; call < 9; ++call) {
+            const Philox r = philox4x32_10((uint32_t)id, (uint32_t)(id >> 32), (uint32_t)call, 0u, k0, k1);
+            u[2 * call] = u53(r.c[0], r.c[1]);
+            u[2 * call + 1] = u53(r.c[2], r.c[3]);
+        }
+        // u[0..8]: A; u[9]: s; u[10..17]: four Box-Muller pairs -> q (4), u (3)
+        double z[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double rr = sqrt(-2.0 * log(1.0 - u[10 + 2 * k]));
+            double sn, cs;
+            sincospi(2.0 * u[11 + 2 * k], &sn, &cs);
+            z[2 * k] = rr * cs;
+            z[2 * k + 1] = rr * sn;
+        }
+        const double qn = rsqrt(z[0] * z[0] + z[1] * z[1] + z[2] * z[2] + z[3] * z[3]);
+        const double w = z[0] * qn, x = z[1] * qn, y = z[2] * qn, zz = z[3] * qn;
+        const double R[9] = {1 - 2 * (y * y + zz * zz), 2 * (x * y - w * zz), 2 * (x * zz + w * y),
+                             2 * (x * y + w * zz), 1 - 2 * (x * x + zz * zz), 2 * (y * zz - w * x),
+                             2 * (x * zz - w * y), 2 * (y * zz + w * x), 1 - 2 * (x * x + y * y)};
+        const double un = rsqrt(z[4] * z[4] + z[5] * z[5] + z[6] * z[6]);
+        const double s = lo + (hi - lo) * u[9];
+        double c[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) c[d] = (u[d] + u[3 + d] + u[6 + d]) * (1.0 / 3.0);
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double b = R[3 * d] * (u[3 * v] - c[0]) + R[3 * d + 1] * (u[3 * v + 1] - c[1]) +
+                                 R[3 * d + 2] * (u[3 * v + 2] - c[2]) + c[d] + s * z[4 + d] * un;
+                planes[(int64_t)(3 * v + d) * n + i] = u[3 * v + d];
+                planes[(int64_t)(9 + 3 * v + d) * n + i] = b;
+            }
+        }
+    }
+}
+
 __global__ void stats_reset_kernel(tc_stats* s) {
     s->iterative = s->comparison = s->fallback = s->degenerate = s->contacts = s->intersecting = 0;
     s->min_distance = __builtin_huge_val();
@@ -1875,6 +1947,18 @@ int64_t tc_fma_probe(int fp64, int64_t blocks, int iters, void* sink, void* stre
     tc::g_launches++;
     if (cudaGetLastError() != cudaSuccess) return -1;
     return (int64_t)2 * 8 * 16 * iters * blocks * tc::BLOCK;
+}
+
+int tc_random_pairs_soa_f64(uint64_t seed, int64_t start, int64_t n, double sep_lo, double sep_hi, double* planes,
+                            void* stream) {
+    if (n < 0 || start < 0 || (n > 0 && !planes)) return TC_EINVAL;
+    if (n == 0) return TC_OK;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)tc::sm_count() * 8);
+    tc::random_pairs_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        seed, start, n, sep_lo, sep_hi, planes);
+    tc::g_launches++;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TC_OK : tc::set_err("random pairs launch", e);
 }
 
 int tc_stats_reset(tc_stats* stats, void* stream) {

@@ -262,3 +262,59 @@ def adversarial_pairs(n_per: int, seed: int = 3):
         As.append(a)
         Bs.append(b)
     return np.concatenate(As), np.concatenate(Bs)
+
+
+# ---------------------------------------------------------------------------
+# Counter-based generator of the same cfg0 distribution (device: the C-ABI
+# tc_random_pairs_soa_f64; this numpy mirror checks it).  Pair i draws nine
+# Philox4x32-10 blocks with counter (i_lo, i_hi, call, 0) and key
+# (seed_lo, seed_hi ^ 0x5EED): 18 uniforms = A (9), s (1), four Box-Muller
+# pairs -> q (4), u (3).  Used for the 2^28-pair cfg4 runs, whose host numpy
+# generation would take minutes.
+# ---------------------------------------------------------------------------
+_PH_M0, _PH_M1, _PH_W0, _PH_W1 = 0xD2511F53, 0xCD9E8D57, 0x9E3779B9, 0xBB67AE85
+
+
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    """Philox4x32-10 on uint32 arrays (broadcast); returns four uint32 arrays."""
+    m32 = np.uint64(0xFFFFFFFF)
+    c = [np.asarray(x, np.uint64) for x in (c0, c1, c2, c3)]
+    k0, k1 = np.uint64(k0), np.uint64(k1)
+    for _ in range(10):
+        p0 = np.uint64(_PH_M0) * c[0]
+        p1 = np.uint64(_PH_M1) * c[2]
+        c = [((p1 >> np.uint64(32)) ^ c[1] ^ k0) & m32, p1 & m32, ((p0 >> np.uint64(32)) ^ c[3] ^ k1) & m32, p0 & m32]
+        k0 = (k0 + np.uint64(_PH_W0)) & m32
+        k1 = (k1 + np.uint64(_PH_W1)) & m32
+    return [x.astype(np.uint32) for x in c]
+
+
+def philox_uniforms(n: int, seed: int = 0, start: int = 0) -> np.ndarray:
+    """(n, 18) uniforms in [0, 1) of pairs [start, start + n) (53-bit, numpy's recipe)."""
+    ids = np.arange(start, start + n, dtype=np.uint64)
+    lo, hi = (ids & np.uint64(0xFFFFFFFF)), ids >> np.uint64(32)
+    k0, k1 = seed & 0xFFFFFFFF, ((seed >> 32) ^ 0x5EED) & 0xFFFFFFFF
+    u = np.empty((n, 18))
+    for call in range(9):
+        r = philox4x32_10(lo, hi, np.full(n, call, np.uint64), np.zeros(n, np.uint64), k0, k1)
+        for j in range(2):
+            a, b = r[2 * j].astype(np.float64), r[2 * j + 1]
+            u[:, 2 * call + j] = (np.floor(a / 32) * 67108864.0 + (b >> np.uint32(6))) / 9007199254740992.0
+    return u
+
+
+def philox_pairs(n: int, seed: int = 0, sep=(-0.05, 0.2), start: int = 0):
+    """(A, B) (n, 3, 3) of the device generator (up to the last ulps of
+    log / sincos / rsqrt, which CUDA and numpy round differently)."""
+    u = philox_uniforms(n, seed, start)
+    A = u[:, :9].reshape(n, 3, 3)
+    r = np.sqrt(-2.0 * np.log(1.0 - u[:, 10::2]))
+    th = 2.0 * np.pi * u[:, 11::2]
+    z = np.empty((n, 8))
+    z[:, 0::2] = r * np.cos(th)
+    z[:, 1::2] = r * np.sin(th)
+    q = z[:, :4] / np.linalg.norm(z[:, :4], axis=1, keepdims=True)
+    v = z[:, 4:7] / np.linalg.norm(z[:, 4:7], axis=1, keepdims=True)
+    s = sep[0] + (sep[1] - sep[0]) * u[:, 9]
+    c = A.mean(axis=1, keepdims=True)
+    return A, rotate_about(A, c, rotation_matrices(q), s[:, None] * v)

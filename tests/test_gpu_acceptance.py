@@ -203,7 +203,7 @@ def test_host_pipeline_staging(layout, real):
     hs = _abi.TcStats(0, 0, 0, 0, 0, 0, float("inf"))
     prm = _abi.params_struct(p, _abi.TC_STRICT | _abi.TC_EMIT_IDS)
     host = getattr(_abi.load(), "tc_run_host_f64" if real == "float64" else "tc_run_host_f32")
-    rc = host(2, *(ptr(x) for x in ins), ctypes.byref(prm),
+    rc = host(2, ptr(ins[0]), ptr(ins[1]), n, ptr(ins[2]), ptr(ins[3]), ctypes.byref(prm),
               *(ptr(out[k]) for k in ("distance", "point_a", "point_b", "bary_a", "bary_b", "kind", "ids")),
               ctypes.byref(hs))
     assert rc == 0
@@ -212,3 +212,30 @@ def test_host_pipeline_staging(layout, real):
     assert [hs.iterative, hs.comparison, hs.fallback, hs.contacts] == \
         [ds["iterative"], ds["comparison"], ds["fallback"], ds["contacts"]]
     assert hs.min_distance == ds["min_distance"]
+
+
+def test_bench_multi_rank_path_on_one_gpu():
+    """bench.py --gpus 2 launches two ranks itself (torch.distributed.run);
+    with --share-gpu both run on cuda:0 (a functional check of the N-rank
+    path, gloo for the stats all-gather, not a measurement): n_gpus is 2 and
+    the whole-job tallies equal a one-rank run over the same pairs, for the
+    cfg1 weak-scaling headline and the cfg4 strong-scaling object."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    common = ["--steps", "3", "--warmup", "3", "--no-extras", "--cfg4-n", "200003"]
+
+    def run(extra):
+        r = subprocess.run([sys.executable, str(root / "bench.py"), *common, *extra], capture_output=True, text=True,
+                           timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        return json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+
+    two = run(["--gpus", "2", "--backend", "gloo", "--share-gpu", "--n", "65536"])
+    one = run(["--n", "131072"])
+    assert two["n_gpus"] == 2 and one["n_gpus"] == 1
+    assert two["stats"] == one["stats"]
+    assert two["configs"]["cfg4_strong"]["stats"] == one["configs"]["cfg4_strong"]["stats"]
+    assert two["configs"]["cfg4_strong"]["pairs_total"] == 200003
