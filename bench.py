@@ -180,7 +180,7 @@ def run_reference(args, rank, world):
     import oracle
     from paper_2105_12415_b200 import workloads as W
     oracle.build()
-    n_all = args.n
+    n_all = args.pairs
     sample = min(n_all, max(-(-n_all // max(args.steps, 1)), 1 << 20))
     p = oracle.make_params(**PARAMS)
     A, B = W.random_pairs_mp(n_all, seed=0, sep=SEP)
@@ -240,7 +240,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_PAIRS, help="pairs per GPU (cfg1)")
+    ap.add_argument("--pairs", type=int, default=N_PAIRS, help="pairs per GPU (cfg1)")
     ap.add_argument("--cfg4-n", type=int, default=CFG4_PAIRS, help="pairs in total (cfg4 strong scaling)")
     ap.add_argument("--strict", action="store_true", help="time the bit-exact TC_STRICT build")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu baseline / variant table / configs")
@@ -272,7 +272,7 @@ def main():
         else:
             dist.init_process_group("gloo")
     lib = _abi.load()
-    n, start, sep = args.n, rank * args.n, SEP
+    n, start, sep = args.pairs, rank * args.pairs, SEP
 
     # ---- inputs: this rank's range of the chunked generator, SoA planes in HBM
     # (generated on all host cores in slices, uploaded slice by slice)

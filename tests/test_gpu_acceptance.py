@@ -233,8 +233,8 @@ def test_bench_multi_rank_path_on_one_gpu():
         assert r.returncode == 0, r.stderr[-3000:]
         return json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
 
-    two = run(["--gpus", "2", "--backend", "gloo", "--share-gpu", "--n", "65536"])
-    one = run(["--n", "131072"])
+    two = run(["--gpus", "2", "--backend", "gloo", "--share-gpu", "--pairs", "65536"])
+    one = run(["--pairs", "131072"])
     assert two["n_gpus"] == 2 and one["n_gpus"] == 1
     assert two["stats"] == one["stats"]
     assert two["configs"]["cfg4_strong"]["stats"] == one["configs"]["cfg4_strong"]["stats"]
