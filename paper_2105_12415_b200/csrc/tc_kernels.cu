@@ -224,21 +224,55 @@ __device__ __forceinline__ void run_iterative(const T* slot, const R* A, const R
     run_iterative(SmemTri<R>{slot, bs}, SmemTri<R>{slot + 9 * bs, bs}, A, B, eps_fn, kp, r);
 }
 
+// L2 eviction-priority hints for the result stores (TC_OUT_HINT): the hybrid
+// writes every lane's tile result at once and rewrites the open pairs' rows
+// after their fallback, several tiles later.  Tile stores of open pairs can
+// carry evict_last (their sectors stay in L2 until the rewrite, which then
+// needs no DRAM read-modify-write), the fallback's final stores evict_first.
+#ifndef TC_OUT_HINT
+#define TC_OUT_HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy(bool last) {
+    uint64_t p;
+    if (last) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_hint(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint(int8_t* p, int8_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.b8 [%0], %1, %2;" ::"l"(p), "h"((short)v), "l"(pol) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void st_col(T* p, T v, bool hint, uint64_t pol) {
+    if (hint) st_hint(p, v, pol);
+    else *p = v;
+}
+
 template <bool SOA, class R, typename T>
-__device__ __forceinline__ void store_rec(const Args<T>& a, int64_t i, const Rec<R>& r) {
+__device__ __forceinline__ void store_rec(const Args<T>& a, int64_t i, const Rec<R>& r, bool hint = false,
+                                          uint64_t pol = 0) {
     const int64_t n = a.n;
-    if (a.distance) a.distance[i] = val(r.distance);
-    if (a.kind) a.kind[i] = (int8_t)r.kind;
+    if (a.distance) st_col(a.distance + i, val(r.distance), hint, pol);
+    if (a.kind) st_col(a.kind + i, (int8_t)r.kind, hint, pol);
     if (SOA) {
-        if (a.pa) { a.pa[i] = val(r.pa[0]); a.pa[n + i] = val(r.pa[1]); a.pa[2 * n + i] = val(r.pa[2]); }
-        if (a.pb) { a.pb[i] = val(r.pb[0]); a.pb[n + i] = val(r.pb[1]); a.pb[2 * n + i] = val(r.pb[2]); }
-        if (a.ba) { a.ba[i] = val(r.ba[0]); a.ba[n + i] = val(r.ba[1]); }
-        if (a.bb) { a.bb[i] = val(r.bb[0]); a.bb[n + i] = val(r.bb[1]); }
+        if (a.pa) { st_col(a.pa + i, val(r.pa[0]), hint, pol); st_col(a.pa + n + i, val(r.pa[1]), hint, pol);
+                    st_col(a.pa + 2 * n + i, val(r.pa[2]), hint, pol); }
+        if (a.pb) { st_col(a.pb + i, val(r.pb[0]), hint, pol); st_col(a.pb + n + i, val(r.pb[1]), hint, pol);
+                    st_col(a.pb + 2 * n + i, val(r.pb[2]), hint, pol); }
+        if (a.ba) { st_col(a.ba + i, val(r.ba[0]), hint, pol); st_col(a.ba + n + i, val(r.ba[1]), hint, pol); }
+        if (a.bb) { st_col(a.bb + i, val(r.bb[0]), hint, pol); st_col(a.bb + n + i, val(r.bb[1]), hint, pol); }
     } else {
-        if (a.pa) { a.pa[3 * i] = val(r.pa[0]); a.pa[3 * i + 1] = val(r.pa[1]); a.pa[3 * i + 2] = val(r.pa[2]); }
-        if (a.pb) { a.pb[3 * i] = val(r.pb[0]); a.pb[3 * i + 1] = val(r.pb[1]); a.pb[3 * i + 2] = val(r.pb[2]); }
-        if (a.ba) { a.ba[2 * i] = val(r.ba[0]); a.ba[2 * i + 1] = val(r.ba[1]); }
-        if (a.bb) { a.bb[2 * i] = val(r.bb[0]); a.bb[2 * i + 1] = val(r.bb[1]); }
+        if (a.pa) { st_col(a.pa + 3 * i, val(r.pa[0]), hint, pol); st_col(a.pa + 3 * i + 1, val(r.pa[1]), hint, pol);
+                    st_col(a.pa + 3 * i + 2, val(r.pa[2]), hint, pol); }
+        if (a.pb) { st_col(a.pb + 3 * i, val(r.pb[0]), hint, pol); st_col(a.pb + 3 * i + 1, val(r.pb[1]), hint, pol);
+                    st_col(a.pb + 3 * i + 2, val(r.pb[2]), hint, pol); }
+        if (a.ba) { st_col(a.ba + 2 * i, val(r.ba[0]), hint, pol); st_col(a.ba + 2 * i + 1, val(r.ba[1]), hint, pol); }
+        if (a.bb) { st_col(a.bb + 2 * i, val(r.bb[0]), hint, pol); st_col(a.bb + 2 * i + 1, val(r.bb[1]), hint, pol); }
     }
     if (a.ids) {
         uint8_t* p = a.ids + 4 * i;
@@ -344,12 +378,28 @@ __device__ __forceinline__ Scratch<R> thread_scratch() {
 }
 // The calling thread's planar shared-memory slot for the pair under
 // comparison (18 coordinates, stride BLOCK), after the crossing scratch.
+// Timing-only experiment knobs (wrong results): TC_X_STAGE_HOT re-reads queued
+// pairs from a small hot region, TC_X_TILE_HOT loads every tile from one, to
+// bound what hiding those loads' latency could gain.
+#ifndef TC_X_STAGE_HOT
+#define TC_X_STAGE_HOT 0
+#endif
+#ifndef TC_X_TILE_HOT
+#define TC_X_TILE_HOT 0
+#endif
+#ifndef TC_X_NOSTORE
+#define TC_X_NOSTORE 0
+#endif
 template <bool SOA, int BS, class R, typename T>
 __device__ __forceinline__ void stage_pair(const Args<T>& a, int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps,
                                            T* slot) {
     constexpr int bs = BS;
+    if (TC_X_STAGE_HOT) j &= 1023;
+#ifndef TC_X_STAGE_NONE
+#define TC_X_STAGE_NONE 0
+#endif
 #pragma unroll
-    for (int k = 0; k < 9; ++k) {
+    for (int k = 0; k < 9 * (1 - TC_X_STAGE_NONE); ++k) {
         slot[k * bs] = __ldg(SOA ? a.tri_a + k * a.n + j : a.tri_a + 9 * j + k);
         slot[(9 + k) * bs] = __ldg(SOA ? a.tri_b + k * a.n + j : a.tri_b + 9 * j + k);
     }
@@ -432,7 +482,10 @@ struct FlatSource {
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
         stage_pair<SOA, BS>(a, j, A, B, eps, slot);
     }
-    __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const { store_rec<SOA>(a, j, r); }
+    __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const {
+        if (TC_OUT_HINT) store_rec<SOA>(a, j, r, true, l2_policy(false));
+        else store_rec<SOA>(a, j, r);
+    }
     __device__ __forceinline__ void store_ids01(int64_t j, uint32_t ids) const {
         a.ids[4 * j] = (uint8_t)(ids & 0xFF);
         a.ids[4 * j + 1] = (uint8_t)((ids >> 8) & 0xFF);
@@ -606,6 +659,12 @@ __global__ void __launch_bounds__(BS_ITER, TC_MINB(BS_ITER, TC_ITER_MINB)) itera
 // phase 1 in-tile on the compacted open lanes, straight from the owners'
 // shared-memory slots, saves the re-read of queued pairs but idles half the
 // warps: measured 8% slower on cfg1.)
+// TC_TILE_CPASYNC: the next tile's pair is copied into a second per-thread
+// shared-memory slot by cp.async while the current tile computes, so a tile
+// starts from shared memory instead of waiting for its global loads.
+#ifndef TC_TILE_CPASYNC
+#define TC_TILE_CPASYNC 0
+#endif
 template <typename T, bool STRICT, bool SOA>
 __global__ void __launch_bounds__(BS_HYB, TC_MINB(BS_HYB, TC_HYBRID_MINB)) hybrid_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
@@ -616,29 +675,56 @@ __global__ void __launch_bounds__(BS_HYB, TC_MINB(BS_HYB, TC_HYBRID_MINB)) hybri
     __syncthreads();
     const int64_t ntiles = (a.n + BS_HYB - 1) / BS_HYB;
     T* const slot = thread_slot<T>(SCR * BS_HYB);  // the comparison phases' pair slot, free here
+    T* const nslot = thread_slot<T>((SCR + SLOT) * BS_HYB);  // TC_TILE_CPASYNC: the next tile's pair
+    if (TC_TILE_CPASYNC) async_pair<SOA, BS_HYB>(a, (int64_t)blockIdx.x * BS_HYB + threadIdx.x, nslot);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        prefetch_tile<SOA, BS_HYB>(a, tile + gridDim.x);
+        if (!TC_TILE_CPASYNC) prefetch_tile<SOA, BS_HYB>(a, tile + gridDim.x);
         const int64_t i = tile * BS_HYB + threadIdx.x;
         bool enq = false;
+        if (TC_TILE_CPASYNC) cp_async_wait_all();
         if (i < a.n) {
             R A[9], B[9], eps;
-            load_pair<SOA>(a, i, A, B, eps);
+            if (TC_TILE_CPASYNC) {
+#pragma unroll
+                for (int k = 0; k < 9; ++k) {
+                    A[k] = R(nslot[k * BS_HYB]);
+                    B[k] = R(nslot[(9 + k) * BS_HYB]);
+                }
+                eps = R(a.eps ? a.eps[i] : a.eps_scalar);
+            } else {
+                load_pair<SOA>(a, TC_X_TILE_HOT ? (i & 4095) : i, A, B, eps);
+            }
             stash_pair<BS_HYB>(slot, A, B);
+            // (the stash consumed the slot's values: the next copy may land)
+            if (TC_TILE_CPASYNC) async_pair<SOA, BS_HYB>(a, i + (int64_t)gridDim.x * BS_HYB, nslot);
             Rec<R> r;
-            run_iterative<BS_HYB>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
+#ifndef TC_X_RELOAD_GLOBAL
+#define TC_X_RELOAD_GLOBAL 0
+#endif
+            if (TC_X_RELOAD_GLOBAL && SOA)
+                run_iterative(GlobalTri<R>{a.tri_a + i, a.n}, GlobalTri<R>{a.tri_b + i, a.n}, A, B,
+                              [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
+            else
+                run_iterative<BS_HYB>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
             tl.iterative++;
             // open pairs are queued; the phase-1 batches screen them for
             // degenerate triangles (drain<SCREEN>)
             enq = r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i]);
             // every lane stores its tile result now (open pairs a placeholder
             // the fallback overwrites), so output sectors are written whole
-            store_rec<SOA>(a, i, r);
+            if (!TC_X_NOSTORE) {
+                if (TC_OUT_HINT) store_rec<SOA>(a, i, r, TC_OUT_HINT == 2 || enq, l2_policy(true));
+                else store_rec<SOA>(a, i, r);
+            }
             if (!enq) tl.result(r);
+        } else if (TC_TILE_CPASYNC) {
+            asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count uniform
         }
         push(Q.q1, &Q.n1, enq, i);
         __syncthreads();
         drain<true, R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
+    if (TC_TILE_CPASYNC) cp_async_wait_all();
     drain<true, R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
     tl.flush<true>(a.stats);
 }
@@ -1224,7 +1310,10 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         k<<<(unsigned)grid_for(k, a.n, smem, BS_ITER), BS_ITER, smem, s>>>(a);
     } else {
         auto k = hybrid_kernel<T, STRICT, SOA>;
-        const size_t smem = scratch_bytes<T>(BS_HYB);
+#ifndef TC_X_PAD
+#define TC_X_PAD 0
+#endif
+        const size_t smem = scratch_bytes<T>(BS_HYB) + (TC_TILE_CPASYNC ? sizeof(T) * SLOT * BS_HYB : 0) + TC_X_PAD;
         k<<<(unsigned)grid_for(k, a.n, smem, BS_HYB), BS_HYB, smem, s>>>(a);
     }
     g_launches++;

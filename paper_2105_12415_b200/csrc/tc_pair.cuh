@@ -225,6 +225,19 @@ struct SmemTri {
     }
 };
 
+// One triangle of a planar (SoA) global array, read through the read-only
+// path: coordinate k at p[k * stride].
+template <class R>
+struct GlobalTri {
+    const typename Store<R>::type* p;
+    int64_t stride;
+    __device__ __forceinline__ R operator[](int k) const { return R(__ldg(p + k * stride)); }
+    __device__ __forceinline__ void vertex(int k, R* v) const {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) v[i] = R(__ldg(p + (3 * k + i) * stride));
+    }
+};
+
 // RK/geometry.py:68-75 degenerate_mask through an accessor (e.g. a pair kept
 // in shared memory, so the caller's registers are not pinned by it).
 template <class R, class Tri>
@@ -696,6 +709,25 @@ __device__ __forceinline__ float clip0_hi(float x, float hi) {
 template <typename T>
 __device__ __forceinline__ Strict<T> clip0_hi(Strict<T> x, Strict<T> hi) { return clip0_hi(x.v, hi.v); }
 
+// Fast build's coordinate clip.  With TC_LOWCLIP_IMNMX the lower clip is one
+// integer max on the high word (a negative x becomes +0 in the high word with
+// its low word kept: a positive denormal below 2^-1022 instead of +0, which
+// every later use rounds away), then the upper clip's compare and select:
+// 5 issue slots instead of 7 (tools/sweep_probe2.cu: 147 -> 142 cycles per
+// warp-sweep).  Not bitwise: strict mode keeps clip0_hi.
+#ifndef TC_LOWCLIP_IMNMX
+#define TC_LOWCLIP_IMNMX 1
+#endif
+__device__ __forceinline__ double clip0_hi_fast(double x, double hi) {
+#if TC_LOWCLIP_IMNMX
+    const double m = __hiloint2double(max(__double2hiint(x), 0), __double2loint(x));
+    return (m < hi) ? m : hi;
+#else
+    return clip0_hi(x, hi);
+#endif
+}
+__device__ __forceinline__ float clip0_hi_fast(float x, float hi) { return clip0_hi(x, hi); }
+
 // clip(t, -xb, xa) for xa, xb >= 0 (the fast build's box mode): clip the
 // magnitude against the bound on t's side, keep t's sign.
 __device__ __forceinline__ double clip_sym(double t, double xb, double xa) {
@@ -888,20 +920,20 @@ struct GramSolver {
 
     __device__ __forceinline__ void sweep() {
         R t, s;
-        t = clip0_hi(x0 - g0 * r0, hi_of(x1));
+        t = clip0_hi_fast(x0 - g0 * r0, hi_of(x1));
         s = t - x0; x0 = t;
         g0 += s * G00; g1 += s * G01; g3 += s * G03; g4 += s * G04;
-        t = clip0_hi(x1 - g1 * r1, hi_of(x0));
+        t = clip0_hi_fast(x1 - g1 * r1, hi_of(x0));
         s = t - x1; x1 = t;
         g0 += s * G01; g1 += s * G11; g3 += s * G13; g4 += s * G14;
         t = -(g1 - g0) * r3a;
         t = BOX ? clip_sym(t, x1, x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
         x0 = x0 - t; x1 = x1 + t;
         g0 += t * SA0; g1 += t * SA1; g3 += t * SA3; g4 += t * SA4;
-        t = clip0_hi(x2 - g3 * r2, hi_of(x3));
+        t = clip0_hi_fast(x2 - g3 * r2, hi_of(x3));
         s = t - x2; x2 = t;
         g0 += s * G03; g1 += s * G13; g3 += s * G33; g4 += s * G34;
-        t = clip0_hi(x3 - g4 * r3, hi_of(x2));
+        t = clip0_hi_fast(x3 - g4 * r3, hi_of(x2));
         s = t - x3; x3 = t;
         g0 += s * G04; g1 += s * G14; g3 += s * G34; g4 += s * G44;
         t = -(g4 - g3) * r3b;

@@ -91,8 +91,11 @@ def test_blocks_contact_capacity_and_empty(scene):
     torch.cuda.synchronize()
     n = int(out["n_contacts"].item())
     assert n > 3                                       # all counted ...
-    res = PT.sort_contacts(out)
-    assert res["idx"].shape == (3, 3)                  # ... only max_contacts stored
+    with pytest.raises(RuntimeError):                  # ... never a truncated, slot-order dependent subset
+        PT.sort_contacts(out)
+    full = PT.blocks_hybrid(torch.from_numpy(meshes).cuda(), torch.from_numpy(blocks[which]).cuda(),
+                            D.Params(epsilon=6e-2), max_contacts=n)
+    assert PT.sort_contacts(full)["idx"].shape == (n, 3)
     empty = PT.blocks_hybrid(torch.from_numpy(meshes).cuda(), torch.zeros((0, 2), dtype=torch.int32).cuda(),
                              D.Params())
     assert int(empty["n_contacts"].item()) == 0

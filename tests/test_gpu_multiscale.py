@@ -80,26 +80,83 @@ def test_batched_reposed_vs_oracle_bitwise(oracle_lib, real):
     assert (res.stats["iterative"], res.stats["comparison"], res.stats["fallback"]) == tuple(o["counts"][:3])
 
 
-@pytest.mark.parametrize("real", list(DTYPES))
-def test_fast_rounding_close_to_oracle(oracle_lib, real):
-    import ms_oracle
+def _replay_fast(oracle_lib, trees, pairs, dt):
+    """RK/stepping.py:311-368 replayed round by round in Python over the fast
+    device hybrid (device entry point, per-pair halos 0.5 (eps_i + eps_j),
+    fallback only where both sides are mesh triangles).  Every round's results
+    go through the tie-aware checker against the oracle on the same pairings
+    (tests/parity.py: kinds / paths / ids equal except at ties within the
+    north-star tolerance, values within it).  Returns the mesh-level contacts
+    {(pair, src_i, src_j): (point_a, point_b)} and the per-round reports."""
+    import torch
+    import parity
+    from paper_2105_12415_b200 import device as D
 
+    tt = {np.float64: torch.float64, np.float32: torch.float32}[dt]
+    front = [(k, 0, 0) for k in range(len(pairs))]
+    contacts, reports = {}, []
+    while front:
+        f = np.array(front, np.int64)
+        ti = [trees[pairs[k][0]] for k in f[:, 0]]
+        tj = [trees[pairs[k][1]] for k in f[:, 0]]
+        A = np.stack([t["tris"].reshape(-1, 3, 3)[i] for t, i in zip(ti, f[:, 1])]).astype(dt)
+        B = np.stack([t["tris"].reshape(-1, 3, 3)[j] for t, j in zip(tj, f[:, 2])]).astype(dt)
+        ei = np.array([t["eps"][i] for t, i in zip(ti, f[:, 1])], dt)
+        ej = np.array([t["eps"][j] for t, j in zip(tj, f[:, 2])], dt)
+        halo = (dt(0.5) * (ei + ej)).astype(dt)
+        fine_i = np.array([i >= t["n_nodes"] for t, i in zip(ti, f[:, 1])])
+        fine_j = np.array([j >= t["n_nodes"] for t, j in zip(tj, f[:, 2])])
+        both = fine_i & fine_j
+        out = D.run("hybrid", torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), D.Params(),
+                    eps=torch.from_numpy(halo).cuda(), allow=torch.from_numpy(both.astype(np.uint8)).cuda(),
+                    strict=False, ids=True)
+        got = {k: v.cpu().numpy() for k, v in out.items()}
+        rep = parity.compare_fast(oracle_lib, "hybrid", A, B, {}, got, dt, eps=halo, allow=both)
+        reports.append(rep)
+        nxt = []
+        for r, (k, i, j) in enumerate(front):
+            kd = got["kind"][r]
+            if both[r]:
+                if kd == 1:
+                    contacts[(k, i - ti[r]["n_nodes"], j - tj[r]["n_nodes"])] = (got["point_a"][r], got["point_b"][r])
+                continue
+            if kd in (1, 2):
+                ci = [i] if fine_i[r] else list(ti[r]["child_ids"][ti[r]["child_off"][i]:ti[r]["child_off"][i + 1]])
+                cj = [j] if fine_j[r] else list(tj[r]["child_ids"][tj[r]["child_off"][j]:tj[r]["child_off"][j + 1]])
+                nxt += [(k, a, b) for a in ci for b in cj]
+        front = nxt
+    return contacts, reports
+
+
+@pytest.mark.parametrize("real", list(DTYPES))
+def test_fast_traversal_tie_aware(oracle_lib, real):
+    """Fast (FMA-contracted) traversal: every decision of every round checked
+    against the oracle with the tie classifier (no contact-set slack), and the
+    fused device traversal equal, bit for bit, to the round-by-round replay
+    over the device hybrid."""
     g = load(real)
     dt = DTYPES[real]
     trees, pairs = _batched_scene(g, dt, poses=3, seed=11)
+    contacts, reports = _replay_fast(oracle_lib, trees, [tuple(p) for p in pairs], dt)
+    for rep in reports:
+        assert rep["ok"], rep
+    assert sum(r["n"] for r in reports) > 1000 and len(contacts) > 50
     res, cp = _run(trees, pairs, dt, strict=False)
-    o = ms_oracle.multiscale(trees, pairs, oracle_lib.make_params(), dtype=dt)
-    key = lambda p, s: set(map(tuple, np.concatenate([p, s], 1).tolist()))  # noqa: E731
-    got, ref = key(cp["pair"], cp["source"]), key(o["pair"], o["source"])
-    # halo-boundary verdicts may flip under FMA rounding: a handful at most
-    assert len(got ^ ref) <= max(2, len(ref) // 50), (len(got ^ ref), len(ref))
-    common = sorted(got & ref)
-    ig = {k: n for n, k in enumerate(map(tuple, np.concatenate([cp["pair"], cp["source"]], 1).tolist()))}
-    ir = {k: n for n, k in enumerate(map(tuple, np.concatenate([o["pair"], o["source"]], 1).tolist()))}
-    a = cp["position"][[ig[k] for k in common]]
-    b = o["position"][[ir[k] for k in common]]
-    tol = 1e-9 if dt == np.float64 else 2e-3
-    assert np.abs(a - b).max() <= tol
+    got = {(int(np.nonzero((pairs == p).all(1))[0][0]), int(s[0]), int(s[1])): n
+           for n, (p, s) in enumerate(zip(cp["pair"], cp["source"]))}
+    assert set(got) == set(contacts)
+    order = [got[k] for k in contacts]
+    pa = np.array([contacts[k][0] for k in contacts])
+    pb = np.array([contacts[k][1] for k in contacts])
+    assert np.array_equal(np.sort(order), np.arange(len(order)))
+    keys = list(contacts)
+    # positions from the replay's points, rounded like contact_points
+    from paper_2105_12415_b200.contact import contact_from_segment_batch
+    ea = np.array([cp["eps"][got[k]][0] for k in keys])
+    eb = np.array([cp["eps"][got[k]][1] for k in keys])
+    pos, nrm = contact_from_segment_batch(pa, pb, ea, eb)
+    assert pos.astype(dt).tobytes() == cp["position"][order].tobytes()
+    assert nrm.astype(dt).tobytes() == cp["normal"][order].tobytes()
 
 
 def test_capacity_and_empty():
@@ -108,8 +165,11 @@ def test_capacity_and_empty():
     trees = [tree(g, sc, "i"), tree(g, sc, "j")]
     res, _ = _run(trees, np.zeros((0, 2), np.int64), np.float64)
     assert res.n_contacts == 0 and not res.checks.any()
-    res, _ = _run(trees, [(0, 1)], np.float64, max_contacts=3)
-    assert res.n_contacts == g[f"{sc}_source"].shape[0] and res.pair.size == 3
+    # a contact list sized below the count is re-run with room for every
+    # contact: never a truncated (atomic-order dependent) subset
+    res, cp = _run(trees, [(0, 1)], np.float64, max_contacts=3)
+    assert res.n_contacts == g[f"{sc}_source"].shape[0] == res.pair.size
+    assert np.array_equal(cp["source"], g[f"{sc}_source"])
 
 
 @pytest.mark.parametrize("real", list(DTYPES))

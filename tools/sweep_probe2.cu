@@ -87,7 +87,33 @@ struct Sw {
         const bool below = !(t > lo), above = !(t < xa);
         return below ? lo : (above ? xa : t);
     }
+    __device__ __forceinline__ static double sclip(double sr, double x, double hs) {
+        // clamp(sr, -x, hs) with independent compares of the raw step
+        const double lo = -x;
+        const bool below = !(sr > lo), above = !(sr < hs);
+        return below ? lo : (above ? hs : sr);
+    }
+    __device__ __forceinline__ void sweep_s() {
+        double t, s;
+        s = sclip(-g0 * r0, x0, (1.0 - x1) - x0); x0 += s;
+        g0 += s * G00; g1 += s * G01; g3 += s * G03; g4 += s * G04;
+        s = sclip(-g1 * r1, x1, (1.0 - x0) - x1); x1 += s;
+        g0 += s * G01; g1 += s * G11; g3 += s * G13; g4 += s * G14;
+        t = -(g1 - g0) * r3a;
+        t = csym(t, x1, x0);
+        x0 = x0 - t; x1 = x1 + t;
+        g0 += t * SA0; g1 += t * SA1; g3 += t * SA3; g4 += t * SA4;
+        s = sclip(-g3 * r2, x2, (1.0 - x3) - x2); x2 += s;
+        g0 += s * G03; g1 += s * G13; g3 += s * G33; g4 += s * G34;
+        s = sclip(-g4 * r3, x3, (1.0 - x2) - x3); x3 += s;
+        g0 += s * G04; g1 += s * G14; g3 += s * G34; g4 += s * G44;
+        t = -(g4 - g3) * r3b;
+        t = csym(t, x3, x2);
+        x2 = x2 - t; x3 = x3 + t;
+        g0 += t * SB0; g1 += t * SB1; g3 += t * SB3; g4 += t * SB4;
+    }
     __device__ __forceinline__ void sweep() {
+        if (CL == 12) { sweep_s(); return; }
         double t, s;
         t = c0hi(x0 - g0 * r0, 1.0 - x1);
         s = t - x0; x0 = t;
@@ -167,17 +193,18 @@ void run_lat(double* d, const char* name) {
 }
 
 template <int CL, int BS, int MINB>
-void run(double* d, const char* name) {
+void run(double* d, const char* name, size_t smem = 0) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweeps<CL, BS, MINB>, BS, 0);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(sweeps<CL, BS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweeps<CL, BS, MINB>, BS, smem);
     const int blocks = 148 * per_sm * 8, n = 512;
     float best = 1e30f;
     for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(e0);
-        sweeps<CL, BS, MINB><<<blocks, BS>>>(d, n, 0.1);
+        sweeps<CL, BS, MINB><<<blocks, BS, smem>>>(d, n, 0.1);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -196,6 +223,11 @@ void run(double* d, const char* name) {
 int main() {
     double* d;
     cudaMalloc(&d, 8);
+    run<0, 128, 4>(d, "current clips, 16 w/SM (smem-capped)", 56 * 1024);
+    run<0, 128, 4>(d, "current clips, 20 w/SM (smem-capped)", 44 * 1024);
+    run<0, 128, 4>(d, "current clips, 12 w/SM (smem-capped)", 72 * 1024);
+    run<0, 128, 4>(d, "current clips, 8 w/SM (smem-capped)", 110 * 1024);
+    run<3, 128, 4>(d, "IMNMX, 16 w/SM (smem-capped)", 56 * 1024);
     run_lat<0, 128, 4>(d, "current clips");
     run_lat<1, 128, 4>(d, "no clips");
     run_lat<6, 128, 4>(d, "upper clip only");
@@ -211,6 +243,9 @@ int main() {
     run<5, 128, 8>(d, "slide as clip0_hi(x0-t, x0+x1), 32 w/SM");
     run<6, 128, 4>(d, "upper clip only, 24 w/SM");
     run<10, 128, 4>(d, "predicated PTX movs, 24 w/SM");
+    run<12, 128, 4>(d, "step-form clips (s = clamp(-g r, -x, h - x)), 24 w/SM");
+    run<12, 128, 8>(d, "step-form clips, 32 w/SM");
+    run_lat<12, 128, 4>(d, "step-form clips");
     run<11, 128, 4>(d, "IMNMX lower + predicated mov, 24 w/SM");
     run_lat<10, 128, 4>(d, "predicated PTX movs");
     run<7, 128, 4>(d, "int64 upper compare + sign, 24 w/SM");

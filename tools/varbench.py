@@ -1,0 +1,63 @@
+"""Time the hybrid kernel of several library builds on the same device-resident
+inputs (one process; each variants/*.so loaded through its own ctypes handle).
+
+    python tools/varbench.py [--n N] [--dtype f64|f32] [--rounds R] variants/a.so variants/b.so ...
+"""
+import argparse
+import ctypes
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import torch
+from paper_2105_12415_b200 import _abi, device as D, workloads as W
+
+ap = argparse.ArgumentParser()
+ap.add_argument("libs", nargs="+")
+ap.add_argument("--n", type=int, default=1 << 24)
+ap.add_argument("--dtype", default="f64")
+ap.add_argument("--rounds", type=int, default=3)
+ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--strict", action="store_true")
+ap.add_argument("--variant", default="hybrid")
+args = ap.parse_args()
+dt = torch.float64 if args.dtype == "f64" else torch.float32
+n = args.n
+planes = torch.empty((18, n), dtype=torch.float64, device="cuda")
+lib0 = _abi.load()
+_abi.check(lib0.tc_random_pairs_soa_f64(0, 0, n, -0.1, 0.5, ctypes.c_void_p(planes.data_ptr()), None), "gen")
+planes = planes.to(dt)
+ta, tb = planes[:9], planes[9:]
+out = D.alloc_outputs(n, dt, "cuda", soa=True)
+stats = D.new_stats()
+P = D.Params(n_iterative=16, epsilon=1e-6)
+flags = _abi.TC_SOA | (_abi.TC_STRICT if args.strict else 0)
+p = _abi.params_struct(P, flags)
+sfx = "f64" if dt == torch.float64 else "f32"
+libs = [(Path(x).name, _abi.load(x)) for x in args.libs]
+ptr = lambda t: ctypes.c_void_p(t.data_ptr())
+cols = [ptr(out[k]) for k in ("distance", "point_a", "point_b", "bary_a", "bary_b", "kind")]
+res = {name: [] for name, _ in libs}
+stats_of = {}
+for r in range(args.rounds):
+    for name, lib in libs:
+        fn = getattr(lib, f"tc_{args.variant}_{sfx}")
+        call = (lambda: fn(ptr(ta), ptr(tb), n, None, None, ctypes.byref(p), *cols, None, ptr(stats), None)) \
+            if args.variant == "hybrid" else \
+            (lambda: fn(ptr(ta), ptr(tb), n, None, ctypes.byref(p), *cols, None, ptr(stats), None))
+        for _ in range(2):
+            assert call() == 0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        lib.tc_stats_reset(ptr(stats), None)
+        e0.record()
+        for _ in range(args.reps):
+            call()
+        e1.record()
+        torch.cuda.synchronize()
+        res[name].append(e0.elapsed_time(e1) / args.reps)
+        stats_of[name] = D.read_stats(stats)
+for name, ts in res.items():
+    st = stats_of[name]
+    print(f"{name:40s} {min(ts):7.3f} ms  {n / min(ts) / 1e6:8.1f} M pairs/s  (rounds {' '.join(f'{t:.3f}' for t in ts)})"
+          f"  fb {st['fallback'] // (args.reps + 0)} contacts {st['contacts'] // args.reps}", flush=True)
