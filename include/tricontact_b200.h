@@ -240,6 +240,13 @@ int tc_run_host_f32(int variant, const float* tri_a, const float* tri_b, int64_t
                     float* distance, float* point_a, float* point_b, float* bary_a,
                     float* bary_b, int8_t* kind, uint8_t* ids, tc_stats* stats);
 
+/* Pinned host memory for result arrays: tc_run_host_* writes pinned outputs
+ * by DMA directly instead of staging them (the drop-in allocates its
+ * BatchResult columns here).  Blocks are recycled by size; tc_host_alloc
+ * returns NULL on failure (tc_last_error), tc_host_free TC_EINVAL for a
+ * pointer it did not hand out. */
+void* tc_host_alloc(int64_t bytes);
+int tc_host_free(void* p);
 /* Host-pointer versions of the two helpers above (synchronous). */
 int tc_closest_point_triangle_host_f64(const double* points, const double* tris, int64_t n,
                                        double* closest, double* bary);

@@ -1866,6 +1866,79 @@ static int run_host(int variant, const T* tri_a, const T* tri_b, int64_t n, cons
     return TC_OK;
 }
 
+// Pinned host blocks for result arrays (tc_host_alloc / tc_host_free): a
+// caller that allocates its outputs here gets them written by DMA directly
+// (tc_run_host_* sees pinned memory and skips the copy-out staging).  Freed
+// blocks are cached by size (2 MB granules) up to TC_HOST_POOL_MB (default
+// 16 GB), so steady-state calls never pay cudaHostAlloc.
+struct HostPool {
+    std::mutex mu;
+    std::vector<std::pair<size_t, void*>> free_blocks;
+    std::vector<std::pair<void*, size_t>> live;
+    size_t cached = 0;
+    size_t cap() const {
+        const char* v = getenv("TC_HOST_POOL_MB");
+        return (size_t)(v ? atoll(v) : 16384) << 20;
+    }
+};
+static HostPool g_pool;
+
+static void* host_alloc(int64_t bytes) {
+    if (bytes <= 0) return nullptr;
+    const size_t sz = ((size_t)bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1);
+    std::lock_guard<std::mutex> l(g_pool.mu);
+    // best fit among cached blocks of [sz, 2 sz]
+    size_t best = g_pool.free_blocks.size();
+    for (size_t k = 0; k < g_pool.free_blocks.size(); ++k) {
+        const size_t b = g_pool.free_blocks[k].first;
+        if (b >= sz && b <= 2 * sz && (best == g_pool.free_blocks.size() || b < g_pool.free_blocks[best].first))
+            best = k;
+    }
+    if (best < g_pool.free_blocks.size()) {
+        const size_t bsz = g_pool.free_blocks[best].first;
+        void* p = g_pool.free_blocks[best].second;
+        g_pool.free_blocks.erase(g_pool.free_blocks.begin() + best);
+        g_pool.cached -= bsz;
+        g_pool.live.push_back({p, bsz});
+        return p;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaHostAlloc(&p, sz, cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        // release the cache and retry once
+        for (auto& b : g_pool.free_blocks) cudaFreeHost(b.second);
+        g_pool.free_blocks.clear();
+        g_pool.cached = 0;
+        cudaGetLastError();
+        if ((e = cudaHostAlloc(&p, sz, cudaHostAllocPortable)) != cudaSuccess) {
+            set_err("cudaHostAlloc", e);
+            return nullptr;
+        }
+    }
+    g_pool.live.push_back({p, sz});
+    return p;
+}
+
+static int host_free(void* p) {
+    if (!p) return TC_OK;
+    std::lock_guard<std::mutex> l(g_pool.mu);
+    for (size_t k = 0; k < g_pool.live.size(); ++k) {
+        if (g_pool.live[k].first == p) {
+            const size_t sz = g_pool.live[k].second;
+            g_pool.live.erase(g_pool.live.begin() + k);
+            if (g_pool.cached + sz <= g_pool.cap()) {
+                g_pool.free_blocks.push_back({sz, p});
+                g_pool.cached += sz;
+            } else {
+                cudaFreeHost(p);
+            }
+            return TC_OK;
+        }
+    }
+    snprintf(g_err, sizeof(g_err), "tc_host_free: %p was not allocated by tc_host_alloc", p);
+    return TC_EINVAL;
+}
+
 template <typename T>
 static int run_cpt(const T* P, const T* Tr, int64_t n, T* closest, T* bary, void* stream) {
     if (n < 0 || (n > 0 && (!P || !Tr))) return TC_EINVAL;
@@ -2027,6 +2100,9 @@ int tc_allreduce_stats(tc_stats* stats, void* nccl_comm, void* stream) {
     }
     return TC_OK;
 }
+
+void* tc_host_alloc(int64_t bytes) { return tc::host_alloc(bytes); }
+int tc_host_free(void* p) { return tc::host_free(p); }
 
 int64_t tc_fma_probe(int fp64, int64_t blocks, int iters, void* sink, void* stream) {
     if (blocks < 1 || iters < 1 || !sink) return -1;

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 from dataclasses import dataclass
 from enum import IntEnum
 
@@ -180,6 +181,35 @@ def _sfx(dtype) -> str:
     return "f32" if np.dtype(dtype) == np.float32 else "f64"
 
 
+_PINNED_MIN = 1 << 16  # pairs; smaller results are plain numpy arrays
+
+
+def _result(n: int) -> BatchResult:
+    """Result columns for n pairs.  Large results live in one pinned host
+    block of the library (tc_host_alloc), which the DMA engines write directly
+    (no staging copy); the block returns to the library's cache when the last
+    column view is garbage-collected.  They are ordinary writeable numpy
+    arrays for the caller."""
+    cols = (("distance", (n,), REAL), ("point_a", (n, 3), REAL), ("point_b", (n, 3), REAL),
+            ("bary_a", (n, 2), REAL), ("bary_b", (n, 2), REAL), ("kind", (n,), np.int8))
+    if n >= _PINNED_MIN:
+        offs, total = [], 0
+        for _, shape, dt in cols:
+            offs.append(total)
+            total += (int(np.prod(shape)) * np.dtype(dt).itemsize + 255) & ~255
+        lib = _abi.load()
+        ptr = lib.tc_host_alloc(total)
+        if ptr:
+            buf = (ctypes.c_char * total).from_address(ptr)
+            fin = weakref.finalize(buf, lib.tc_host_free, ptr)
+            fin.atexit = False  # the process is ending: the OS reclaims the block
+            raw = np.frombuffer(buf, np.uint8)
+            arrs = {name: raw[o:o + int(np.prod(shape)) * np.dtype(dt).itemsize].view(dt).reshape(shape)
+                    for (name, shape, dt), o in zip(cols, offs)}
+            return BatchResult(**arrs)
+    return BatchResult(**{name: np.empty(shape, dt) for name, shape, dt in cols})
+
+
 def _run(variant: str, A, B, eps, params, allow=None):
     """One host-buffer C-ABI call; returns (BatchResult, TcStats, rc).
 
@@ -196,14 +226,7 @@ def _run(variant: str, A, B, eps, params, allow=None):
     n = A.shape[0]
     if B.shape[0] != n:
         raise ValueError("tri_a and tri_b must have the same length")
-    res = BatchResult(
-        kind=np.empty(n, np.int8),
-        distance=np.empty(n, REAL),
-        point_a=np.empty((n, 3), REAL),
-        point_b=np.empty((n, 3), REAL),
-        bary_a=np.empty((n, 2), REAL),
-        bary_b=np.empty((n, 2), REAL),
-    )
+    res = _result(n)
     stats = _abi.TcStats(0, 0, 0, 0, 0, 0, float("inf"))
     if n == 0:
         return res, stats, _abi.TC_OK

