@@ -270,6 +270,11 @@ int64_t tc_fma_probe(int fp64, int64_t blocks, int iters, void* sink, void* stre
  * distribution (numpy mirror: workloads.philox_pairs). */
 int tc_random_pairs_soa_f64(uint64_t seed, int64_t start, int64_t n, double sep_lo, double sep_hi,
                             double* planes, void* stream);
+/* Test knob: cap the CTAs of every persistent launch (0 = the occupancy
+ * maximum).  Changing the CTA count changes which pairs share a CTA's
+ * fallback queues and batches, so result equality across caps exposes
+ * ordering / synchronisation faults (tests/test_gpu_stress.py). */
+void tc_debug_set_max_ctas(int64_t max_ctas);
 /* Number of kernel launches this library has enqueued since load. */
 int64_t tc_launch_count(void);
 

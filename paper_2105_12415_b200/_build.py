@@ -19,6 +19,9 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtricontact_b200.so"
+# TC_DEBUG build: device-side traps on queue overflow / out-of-range indices
+# (tests/test_gpu_stress.py) -- the checks compute-sanitizer would provide
+LIB_DEBUG = PKG / "libtricontact_b200_debug.so"
 SOURCES = [CSRC / "tc_kernels.cu"]
 DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "tricontact_b200.h"]
 
@@ -37,24 +40,39 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def stale() -> bool:
-    if not LIB.exists():
+def stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     return any(p.stat().st_mtime > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
-    """Compile the library (``out``/``defines``: experiment variants, e.g. launch bounds)."""
-    target = Path(out) if out else LIB
-    if out is None and not defines and not force and not stale():
-        return LIB
+def _cmd(target: Path, defines, verbose=False):
     tmp = target.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
-           "-o", str(tmp), *map(str, SOURCES)]
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, target)
-    return target
+    return tmp, [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
+                 "-o", str(tmp), *map(str, SOURCES)]
+
+
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=(), debug=True) -> Path:
+    """Compile the library (``out``/``defines``: experiment variants, e.g. launch
+    bounds); the default build also compiles the TC_DEBUG library, in parallel."""
+    if out is not None or defines:
+        target = Path(out) if out else LIB
+        tmp, cmd = _cmd(target, defines, verbose)
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, target)
+        return target
+    jobs = []
+    targets = [(LIB, ())] + ([(LIB_DEBUG, ("TC_DEBUG=1",))] if debug else [])
+    for target, defs in targets:
+        if force or stale(target):
+            tmp, cmd = _cmd(target, defs, verbose)
+            jobs.append((subprocess.Popen(cmd), tmp, target))
+    for proc, tmp, target in jobs:
+        if proc.wait() != 0:
+            raise subprocess.CalledProcessError(proc.returncode, "nvcc")
+        os.replace(tmp, target)
+    return LIB
 
 
 if __name__ == "__main__":

@@ -97,6 +97,7 @@ constexpr int SLOT = 18;
 #endif
 
 static std::atomic<int64_t> g_launches{0};
+static std::atomic<int64_t> g_max_ctas{0};  // test knob: tc_debug_set_max_ctas
 static thread_local char g_err[512] = "";
 
 static int set_err(const char* what, cudaError_t e) {
@@ -414,13 +415,26 @@ constexpr size_t scratch_bytes(int bs) { return sizeof(T) * (SCR + SLOT) * bs; }
 constexpr int64_t IDS_ONLY = int64_t(1) << 62;
 
 // Warp-aggregated append (all 32 lanes of the warp must call it).
-__device__ __forceinline__ void push(int64_t* q, int* n, bool pred, int64_t v) {
+// TC_DEBUG builds (libtricontact_b200_debug.so, tests/test_gpu_stress.py)
+// trap on any queue overflow, out-of-range queued index or leftover queue
+// entry -- the checks compute-sanitizer would otherwise provide, which this
+// pool does not allow.
+#ifndef TC_DEBUG
+#define TC_DEBUG 0
+#endif
+#define TC_CHECK(cond)                  \
+    do {                                \
+        if (TC_DEBUG && !(cond)) __trap(); \
+    } while (0)
+
+__device__ __forceinline__ void push(int64_t* q, int* n, bool pred, int64_t v, int cap) {
     const unsigned m = __ballot_sync(0xffffffffu, pred);
     if (!m) return;
     const int lane = threadIdx.x & 31;
     int base = 0;
     if (lane == 0) base = atomicAdd(n, __popc(m));
     base = __shfl_sync(0xffffffffu, base, 0);
+    TC_CHECK(base >= 0 && base + __popc(m) <= cap);
     if (pred) q[base + __popc(m & ((1u << lane) - 1u))] = v;
 }
 
@@ -480,6 +494,7 @@ struct FlatSource {
     T* slot;  // the calling thread's pair slot
     __device__ __forceinline__ bool want_ids() const { return a.ids != nullptr; }
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
+        TC_CHECK(j >= 0 && j < a.n);
         stage_pair<SOA, BS>(a, j, A, B, eps, slot);
     }
     __device__ __forceinline__ void store(int64_t j, const Rec<R>& r) const {
@@ -510,6 +525,7 @@ __device__ __forceinline__ void drain(const Src& src, Queues<QB>& Q, Tally& tl, 
     const bool want_ids = src.want_ids();
     while (true) {
         const int c1 = Q.n1, c2 = Q.n2;
+        TC_CHECK(c1 >= 0 && c1 <= 2 * QB && c2 >= 0 && c2 <= 2 * QB);
         __syncthreads();  // everyone has read the counts before they change
         int which = 0;
         if (c1 >= QB || (final_ && c1 > 0)) which = 1;
@@ -565,9 +581,10 @@ __device__ __forceinline__ void drain(const Src& src, Queues<QB>& Q, Tally& tl, 
                 }
             }
         }
-        if (which == 1) push(Q.q2, &Q.n2, push2, e2);
+        if (which == 1) push(Q.q2, &Q.n2, push2, e2, 2 * QB);
         __syncthreads();
     }
+    TC_CHECK(!final_ || (Q.n1 == 0 && Q.n2 == 0));
 }
 
 template <typename T, bool STRICT, bool SOA>
@@ -598,7 +615,7 @@ __global__ void __launch_bounds__(BS_CMP, TC_MINB(BS_CMP, 2)) comparison_kernel(
                 e2 = i;
             }
         }
-        push(Q.q2, &Q.n2, need2, e2);
+        push(Q.q2, &Q.n2, need2, e2, 2 * BS_CMP);
         __syncthreads();
         drain<false, R>(FlatSource<SOA, R, T, BS_CMP>{a, thread_slot<T>(SCR * BS_CMP)}, Q, tl, false, 0u);
     }
@@ -720,7 +737,7 @@ __global__ void __launch_bounds__(BS_HYB, TC_MINB(BS_HYB, TC_HYBRID_MINB)) hybri
         } else if (TC_TILE_CPASYNC) {
             asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count uniform
         }
-        push(Q.q1, &Q.n1, enq, i);
+        push(Q.q1, &Q.n1, enq, i, 2 * BS_HYB);
         __syncthreads();
         drain<true, R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
@@ -802,6 +819,7 @@ struct BlockSource {
     R eps;
     __device__ __forceinline__ bool want_ids() const { return false; }
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& e) const {
+        TC_CHECK(j >= 0 && j < (int64_t)tris * cols);
         const int i = (int)(j / cols), k = (int)(j % cols);
         A.p = mA + i;
         A.stride = tris;
@@ -902,7 +920,7 @@ __global__ void __launch_bounds__(BS_BLK, TC_MINB(BS_BLK, TC_HYBRID_MINB)) block
                     tl.result(r);
                 }
             }
-            push(Q.q1, &Q.n1, enq, p);
+            push(Q.q1, &Q.n1, enq, p, 2 * BS_BLK);
             __syncthreads();
             drain<true, R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
         }
@@ -973,6 +991,7 @@ struct FrontierSource {
     __device__ __forceinline__ bool want_ids() const { return false; }
     __device__ __forceinline__ void stage(int64_t j, SmemTri<R>& A, SmemTri<R>& B, R& eps) const {
         T* slot = thread_slot<T>(SCR * BS_FRONT);
+        TC_CHECK(j >= 0 && j < a.n);
         const int64_t ia = a.fa[j], ib = a.fb[j];
         R X[9], Y[9];
         load_node(a, ia, X);
@@ -1043,7 +1062,7 @@ __global__ void __launch_bounds__(BS_FRONT, TC_MINB(BS_FRONT, TC_HYBRID_MINB)) f
                 tl.result(r);
             }
         }
-        push(Q.q1, &Q.n1, enq, i);
+        push(Q.q1, &Q.n1, enq, i, 2 * BS_FRONT);
         __syncthreads();
         drain<true, R>(src, Q, tl, false, (uint32_t)FLAG_FALLBACK);
     }
@@ -1277,7 +1296,9 @@ static int64_t grid_for(K kernel, int64_t n, size_t smem = 0, int threads = BLOC
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     const int64_t tiles = (n + threads - 1) / threads;
-    const int64_t full = (int64_t)sm_count() * per_sm;
+    int64_t full = (int64_t)sm_count() * per_sm;
+    const int64_t cap = g_max_ctas.load(std::memory_order_relaxed);
+    if (cap > 0 && full > cap) full = cap;
     return tiles < full ? tiles : full;
 }
 
@@ -2108,6 +2129,8 @@ int tc_allreduce_stats(tc_stats* stats, void* nccl_comm, void* stream) {
     }
     return TC_OK;
 }
+
+void tc_debug_set_max_ctas(int64_t max_ctas) { tc::g_max_ctas.store(max_ctas > 0 ? max_ctas : 0); }
 
 void* tc_host_alloc(int64_t bytes) { return tc::host_alloc(bytes); }
 int tc_host_free(void* p) { return tc::host_free(p); }
