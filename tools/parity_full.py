@@ -3,7 +3,7 @@ hybrid on BASELINE.json cfg3 (4 x 2^20 adversarial pairs) and on 2^22 fresh
 cfg1 pairs, against the C oracle with the tie-aware checker of tests/parity.py,
 fp64 and fp32.  Prints one report per (set, dtype).
 
-    python tools/parity_full.py > profiles/r01_parity_full.txt
+    python tools/parity_full.py > profiles/r02_parity_full.txt
 """
 import sys
 import time
