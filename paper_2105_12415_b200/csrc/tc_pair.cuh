@@ -100,30 +100,47 @@ __device__ __forceinline__ int region_params(R d1, R d2, R d3, R d4, R d5, R d6,
     const R vb = d5 * d2 - d1 * d6;
     const R va = d3 * d6 - d5 * d4;
     const R n43 = d4 - d3, n56 = d5 - d6;
-    int region;
-    if (d1 <= R(0) && d2 <= R(0)) region = 0;
-    else if (d3 >= R(0) && d4 <= d3) region = 1;
-    else if (vc <= R(0) && d1 >= R(0) && d3 <= R(0)) region = 2;
-    else if (d6 >= R(0) && d5 <= d6) region = 3;
-    else if (vb <= R(0) && d2 >= R(0) && d6 <= R(0)) region = 4;
-    else if (va <= R(0) && n43 >= R(0) && n56 >= R(0)) region = 5;
-    else region = 6;
-    // numerator / denominator of the region's parameter(s)
-    R num = R(1), den = R(1);
-    if (region == 2) { num = d1; den = d1 - d3; }
-    if (region == 4) { num = d2; den = d2 - d6; }
-    if (region == 5) { num = n43; den = n43 + n56; }
-    if (region == 6) { num = vb; den = (va + vb) + vc; }
-    den = (den == R(0)) ? R(1) : den;
-    const R q1 = divv(num, den);
-    u = R(0);
-    w = R(0);
-    if (region == 1) u = R(1);
-    if (region == 2) u = q1;
-    if (region == 3) w = R(1);
-    if (region == 4) w = q1;
-    if (region == 5) { u = R(1) - q1; w = q1; }
-    if (region == 6) { u = q1; w = divv(vc, den); }
+    // The claim conditions, all evaluated (bitwise &: no short-circuit
+    // branches -- a branchy chain diverges across the warp's lanes).
+    // d4 <= d3 and d5 <= d6 are the signs of n43 and n56: fl(a - b) has the
+    // sign of a - b, so this is exact.
+    const bool c0 = le0(d1) & le0(d2);
+    const bool c1 = ge0(d3) & le0(n43);
+    const bool c2 = le0(vc) & ge0(d1) & le0(d3);
+    const bool c3 = ge0(d6) & le0(n56);
+    const bool c4 = le0(vb) & ge0(d2) & le0(d6);
+    const bool c5 = le0(va) & ge0(n43) & ge0(n56);
+    // first claim wins: one-hot region predicates
+    const bool r0 = c0, r1 = !c0 & c1, r2 = !(c0 | c1) & c2, r3 = !(c0 | c1 | c2) & c3;
+    const bool r4 = !(c0 | c1 | c2 | c3) & c4, r5 = !(c0 | c1 | c2 | c3 | c4) & c5;
+    const bool r6 = !(c0 | c1 | c2 | c3 | c4 | c5);
+    int region = selv(c5, 5, 6);
+    region = selv(c4, 4, region);
+    region = selv(c3, 3, region);
+    region = selv(c2, 2, region);
+    region = selv(c1, 1, region);
+    region = selv(c0, 0, region);
+    // numerator / denominator of the region's parameter(s), by selects
+    const R one = R(1), zero = R(0);
+    R num = selv(r6, vb, one), den = selv(r6, (va + vb) + vc, one);
+    num = selv(r5, n43, num); den = selv(r5, n43 + n56, den);
+    num = selv(r4, d2, num);  den = selv(r4, d2 - d6, den);
+    num = selv(r2, d1, num);  den = selv(r2, d1 - d3, den);
+    den = selv(den == zero, one, den);
+    R q1, qw;
+    if constexpr (IsStrict<R>::value) {
+        // (IEEE divisions are long: the second one only where it is used)
+        q1 = num / den;
+        qw = zero;
+        if (r6) qw = vc / den;
+    } else {
+        const R r = rcpv(den);
+        q1 = num * r;
+        qw = vc * r;
+    }
+    u = selv(r1, one, selv(r2 | r6, q1, selv(r5, one - q1, zero)));
+    w = selv(r3, one, selv(r4 | r5, q1, selv(r6, qw, zero)));
+    (void)r0;
     return region;
 }
 
@@ -290,14 +307,14 @@ __device__ __forceinline__ int segment_params(const R* p1, const R* q1, const R*
     const R denom = a * e - b * b;
     const bool solve = denom > tiny;
     const R s0 = divv(b * f - c * e, solve ? denom : R(1));
-    s = solve ? clipv(s0, R(0), R(1)) : R(0);
+    s = solve ? clip01(s0) : R(0);
     const R e_safe = (e > tiny) ? e : R(1);
     t = divr(b * s + f, e_safe, re);
     const R a_safe = (a > tiny) ? a : R(1);
-    const bool lo = t < R(0), hi = t > R(1);
-    const R s2 = clipv(divr(lo ? -c : (b - c), a_safe, ra), R(0), R(1));
-    s = (lo || hi) ? s2 : s;
-    t = clipv(t, R(0), R(1));
+    const bool lo = lt0(t), hi = gt1(t);
+    const R s2 = clip01(divr(lo ? -c : (b - c), a_safe, ra));
+    s = (lo | hi) ? s2 : s;
+    t = clip01(t);
     R diff[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
@@ -592,17 +609,26 @@ __device__ __forceinline__ void comparison_phase2_impl(const Tri& A, const Tri& 
         S.putv(3 + k, lb);
         S.putv(9 + k, rcpv(lb > tiny ? lb : R(1)));
     }
-#pragma unroll kUnrollF
-    for (int row = 6; row < 15; ++row) {
-        const int ka = (row - 6) / 3, kb = (row - 6) % 3;
-        R p1[3], q1[3], p2[3], q2[3], s, t, d2;
+    // rows 6 + 3 ka + kb: A's edge ka by runtime index (one address per
+    // outer step), B's three edges at compile-time offsets
+#pragma unroll 1
+    for (int ka = 0; ka < 3; ++ka) {
+        R p1[3], q1[3];
         A.vertex(edge_start(ka), p1);
         A.vertex(edge_end(ka), q1);
-        B.vertex(edge_start(kb), p2);
-        B.vertex(edge_end(kb), q2);
-        const R rak = S.getv(6 + ka), rbk = S.getv(9 + kb), lak = S.getv(ka), lbk = S.getv(3 + kb);
-        const int code = segment_params(p1, q1, p2, q2, rak, rbk, lak, lbk, s, t, d2);
-        if (d2 < best) { best = d2; best_row = row; best_code = code; bp1 = s; bp2 = t; }
+        const R rak = S.getv(6 + ka), lak = S.getv(ka);
+#pragma unroll
+        for (int kb = 0; kb < 3; ++kb) {
+            // (keeps the unrolled tests from being interleaved: the next
+            // test's loads stay behind this point, so one test is live at a time)
+            asm volatile("" ::: "memory");
+            R p2[3], q2[3], s, t, d2;
+            B.vertex(edge_start(kb), p2);
+            B.vertex(edge_end(kb), q2);
+            const R rbk = S.getv(9 + kb), lbk = S.getv(3 + kb);
+            const int code = segment_params(p1, q1, p2, q2, rak, rbk, lak, lbk, s, t, d2);
+            if (d2 < best) { best = d2; best_row = 6 + 3 * ka + kb; best_code = code; bp1 = s; bp2 = t; }
+        }
     }
     o.ids = (uint32_t)best_row | ((uint32_t)best_code << 8);
     if (ids_only) return;
