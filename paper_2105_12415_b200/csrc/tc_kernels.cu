@@ -199,13 +199,15 @@ template <class R, class TA, class TB, class EpsFn>
 __device__ __forceinline__ void run_iterative(const TA& SA, const TB& SB, const R* A, const R* B, EpsFn eps_fn,
                                               const KP<R>& kp, Rec<R>& r) {
     if constexpr (IsStrict<R>::value) {
-        iterative_pair(A, B, eps_fn(), kp, r, [&](R* A0, R* B0) {
+        auto reload = [&](R* A0, R* B0) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
                 A0[k] = SA[k];
                 B0[k] = SB[k];
             }
-        });
+        };
+        if (kp.start_coord >= R(0) && kp.start_coord <= R(1)) iterative_pair<true>(A, B, eps_fn(), kp, r, reload);
+        else iterative_pair<false>(A, B, eps_fn(), kp, r, reload);
     } else {
         auto reload = [&](R* A9, R* B9) {
 #pragma unroll

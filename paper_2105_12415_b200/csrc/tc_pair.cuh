@@ -789,15 +789,27 @@ template <typename T>
 __device__ __forceinline__ Strict<T> clip_sym(Strict<T> t, Strict<T> xb, Strict<T> xa) { return clip_sym(t.v, xb.v, xa.v); }
 
 
+// np.maximum(0, v) for a v that is never -0: +0 when the sign bit is set
+// (a sign test on the integer pipe instead of a DSETP and two selects).
+__device__ __forceinline__ double max0_sign(double v) { return __double2hiint(v) < 0 ? 0.0 : v; }
+__device__ __forceinline__ float max0_sign(float v) { return __float_as_int(v) < 0 ? 0.0f : v; }
+template <typename T>
+__device__ __forceinline__ Strict<T> max0_sign(Strict<T> v) { return max0_sign(v.v); }
+
 // One coordinate substep (RK/kernels.py:531-536): preconditioned descent on
 // the quadratic part, then the clip to [0, max(0, 1 - max(x_partner, 0))].
-// `box`: the fast build's shortcut when start_coord lies in [0, 1] -- every
-// iterate then stays in the box (x >= 0 exactly, x_k + x_partner <= 1 up to
-// an ulp), so the two inner max() are identities up to rounding.
-template <class R>
-__device__ __forceinline__ void coord_step(R& xk, R xp, const R* e, R den, R rcp, R* d, bool box) {
+// BOX (start_coord in [0, 1]): every iterate stays >= 0 -- a clip returns +0
+// or a value in (0, hi] with hi >= +0, and a slide's t lies in [-xb, xa], so
+// xa - t and xb + t round to values >= 0 -- hence max(x_partner, 0) is
+// x_partner bit for bit and the strict build drops it; 1 - x_partner can
+// still round below 0 (x_a + x_b may exceed 1 by an ulp after a slide), so
+// the outer max stays (as a sign test: 1 - x is never -0).  The fast build
+// also drops the outer max (x_k + x_partner <= 1 up to an ulp).
+template <bool BOX, class R>
+__device__ __forceinline__ void coord_step(R& xk, R xp, const R* e, R den, R rcp, R* d) {
     R target = xk - divr(dot3(d, e), den, rcp);
-    if (!IsStrict<R>::value && box) target = clip0_hi(target, R(1) - xp);
+    if (!IsStrict<R>::value && BOX) target = clip0_hi(target, R(1) - xp);
+    else if (BOX) target = clip0_hi(target, max0_sign(R(1) - xp));
     else target = clip0_hi(target, maxv(R(0), R(1) - maxv(xp, R(0))));
     const R step = target - xk;
     xk = target;
@@ -806,10 +818,11 @@ __device__ __forceinline__ void coord_step(R& xk, R xp, const R* e, R den, R rcp
 }
 
 // Slide along the triangle's third edge (RK/kernels.py:537-546).
-template <class R>
-__device__ __forceinline__ void slide_step(R& xa, R& xb, const R* e3, R den3, R rcp3, R* d, bool box) {
+template <bool BOX, class R>
+__device__ __forceinline__ void slide_step(R& xa, R& xb, const R* e3, R den3, R rcp3, R* d) {
     R t = divr(-dot3(d, e3), den3, rcp3);
-    if (!IsStrict<R>::value && box) t = clip_sym(t, xb, xa);
+    if (!IsStrict<R>::value && BOX) t = clip_sym(t, xb, xa);
+    else if (BOX) t = clipv(t, -xb, xa);  // xa, xb >= 0: the max() are identities
     else t = clipv(t, -maxv(xb, R(0)), maxv(xa, R(0)));
     xa = xa - t;
     xb = xb + t;
@@ -823,7 +836,7 @@ __device__ __forceinline__ void slide_step(R& xa, R& xb, const R* e3, R den3, R 
 // The loop carries only the edge directions, reciprocals, x and d; the base
 // vertices A0, B0 are re-read through `reload` (an L1/L2 hit) after the
 // first n-1 sweeps, which keeps the sweep loop's register footprint small.
-template <class R, class Reload>
+template <bool BOX, class R, class Reload>
 __device__ __forceinline__ void iterative_pair(const R* A, const R* B, R eps, const KP<R>& kp, Rec<R>& o,
                                                Reload reload) {
     using T = typename Store<R>::type;
@@ -860,14 +873,13 @@ __device__ __forceinline__ void iterative_pair(const R* A, const R* B, R eps, co
         d[i] = ((((A[i] - B[i]) + x[0] * e1a[i]) + x[1] * e2a[i]) - x[2] * (-ne1b[i])) - x[3] * (-ne2b[i]);
 
     const int n_it = kp.n_iterative;
-    const bool box = kp.start_coord >= R(0) && kp.start_coord <= R(1);
     auto sweep = [&]() {
-        coord_step(x[0], x[1], e1a, den0, r0, d, box);
-        coord_step(x[1], x[0], e2a, den1, r1, d, box);
-        slide_step(x[0], x[1], e3a, den3a, r3a, d, box);
-        coord_step(x[2], x[3], ne1b, den2, r2, d, box);
-        coord_step(x[3], x[2], ne2b, den3, r3, d, box);
-        slide_step(x[2], x[3], ne3b, den3b, r3b, d, box);
+        coord_step<BOX>(x[0], x[1], e1a, den0, r0, d);
+        coord_step<BOX>(x[1], x[0], e2a, den1, r1, d);
+        slide_step<BOX>(x[0], x[1], e3a, den3a, r3a, d);
+        coord_step<BOX>(x[2], x[3], ne1b, den2, r2, d);
+        coord_step<BOX>(x[3], x[2], ne2b, den3, r3, d);
+        slide_step<BOX>(x[2], x[3], ne3b, den3b, r3b, d);
     };
 #pragma unroll 1
     for (int it = 0; it < n_it - 1; ++it) sweep();
