@@ -21,6 +21,7 @@ ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--strict", action="store_true")
 ap.add_argument("--variant", default="hybrid")
+ap.add_argument("--no-fallback", action="store_true", help="hybrid with an all-zero allow mask")
 args = ap.parse_args()
 dt = torch.float64 if args.dtype == "f64" else torch.float32
 n = args.n
@@ -31,6 +32,7 @@ planes = planes.to(dt)
 ta, tb = planes[:9], planes[9:]
 out = D.alloc_outputs(n, dt, "cuda", soa=True)
 stats = D.new_stats()
+no_fb = torch.zeros(n, dtype=torch.uint8, device="cuda")
 P = D.Params(n_iterative=16, epsilon=1e-6)
 flags = _abi.TC_SOA | (_abi.TC_STRICT if args.strict else 0)
 p = _abi.params_struct(P, flags)
@@ -43,7 +45,8 @@ stats_of = {}
 for r in range(args.rounds):
     for name, lib in libs:
         fn = getattr(lib, f"tc_{args.variant}_{sfx}")
-        call = (lambda: fn(ptr(ta), ptr(tb), n, None, None, ctypes.byref(p), *cols, None, ptr(stats), None)) \
+        allow = ptr(no_fb) if args.no_fallback else None
+        call = (lambda: fn(ptr(ta), ptr(tb), n, None, allow, ctypes.byref(p), *cols, None, ptr(stats), None)) \
             if args.variant == "hybrid" else \
             (lambda: fn(ptr(ta), ptr(tb), n, None, ctypes.byref(p), *cols, None, ptr(stats), None))
         for _ in range(2):
