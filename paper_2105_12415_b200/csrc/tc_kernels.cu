@@ -78,9 +78,11 @@ constexpr int BS_ITER = TC_BS_ITER, BS_HYB = TC_BS_HYB, BS_CMP = TC_BS_CMP, BS_B
 // resident CTAs per SM of a bs-thread kernel for a register budget given as
 // CTAs of 256 threads (launch bounds)
 #define TC_MINB(bs, n256) ((n256) * 256 / (bs))
-// L2 bulk prefetch of the next tile's inputs at the start of each tile
+// L2 bulk prefetch of the next tile's inputs at the start of each tile: +0.7 %
+// with the round-1 kernels, -0.5 % (fp64) / -1.6 % (fp32) with the round-2
+// fallback phases (tools/varbench.py, 2^24 cfg1 pairs): off
 #ifndef TC_PREFETCH
-#define TC_PREFETCH 1
+#define TC_PREFETCH 0
 #endif
 // dynamic shared memory of the comparison phases, per thread (stride BLOCK):
 // [crossing points: SCR values (at most 4 points, see comparison_phase1);
