@@ -67,7 +67,9 @@ def test_criterion_1_fast(oracle_lib, golden_r2):
     got = {}
     for variant in ("comparison", "hybrid"):
         got[variant], _ = run_dev(variant, A, B, "float64", "def", False)
-        rep = parity.compare_fast(oracle_lib, variant, A, B, PARAM_SETS["def"], got[variant], np.float64)
+        # (0 excused pairs measured)
+        rep = parity.compare_fast(oracle_lib, variant, A, B, PARAM_SETS["def"], got[variant], np.float64,
+                                  max_excused=1e-4)
         assert rep["ok"], (variant, rep)
     assert _criterion_1(ref, got["comparison"], got["hybrid"]) == (True, True, 0)
 
@@ -101,7 +103,9 @@ def test_fast_masked_hybrid_random(oracle_lib, real, pname):
     eps = (base * 10.0 ** rng.uniform(-1, 2, len(A))).astype(dt)
     allow = rng.random(len(A)) < 0.5
     got, st = run_dev("hybrid", A, B, real, pname, False, eps=eps, allow=allow)
-    rep = parity.compare_fast(oracle_lib, "hybrid", A, B, PARAM_SETS[pname], got, dt, eps=eps, allow=allow)
+    # excused budget ~2x the measured rate (fp64: 0, fp32: 0.82 %)
+    rep = parity.compare_fast(oracle_lib, "hybrid", A, B, PARAM_SETS[pname], got, dt, eps=eps, allow=allow,
+                              max_excused=1e-4 if dt == np.float64 else 1.5e-2)
     assert rep["ok"], rep
     assert st["fallback"] > 0
 

@@ -62,6 +62,7 @@ def test_cfg3_fast_within_tolerance(oracle_lib, cfg3, real):
         sub = {k: v[sl] for k, v in got.items()}
         # adversarial classes are built around ties (exact touching, crossings
         # through a vertex, near-parallel faces): a larger share of excused ties
+        # (measured worst class: 0.24 % fp64, 2.6 % fp32; budgets ~2x)
         rep = parity.compare_fast(oracle_lib, "hybrid", A[sl].astype(dt), B[sl].astype(dt), pkw, sub, dt,
-                                  max_excused=0.02 if dt == np.float64 else 0.06)
+                                  max_excused=5e-3 if dt == np.float64 else 4e-2)
         assert rep["ok"], f"{name}: {rep}"

@@ -111,7 +111,9 @@ def _replay_fast(oracle_lib, trees, pairs, dt):
                     eps=torch.from_numpy(halo).cuda(), allow=torch.from_numpy(both.astype(np.uint8)).cuda(),
                     strict=False, ids=True)
         got = {k: v.cpu().numpy() for k, v in out.items()}
-        rep = parity.compare_fast(oracle_lib, "hybrid", A, B, {}, got, dt, eps=halo, allow=both)
+        # (measured excused rates: 0.013 % fp64, 0.043 % fp32)
+        rep = parity.compare_fast(oracle_lib, "hybrid", A, B, {}, got, dt, eps=halo, allow=both,
+                                  max_excused=1e-3 if dt == np.float64 else 5e-3)
         reports.append(rep)
         nxt = []
         for r, (k, i, j) in enumerate(front):

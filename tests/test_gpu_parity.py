@@ -242,7 +242,9 @@ def test_fast_vs_oracle_one_million(oracle_lib, real):
     A = A.astype(dt)
     B = B.astype(dt)
     got, _ = run_dev("hybrid", A, B, real, "bl", False)
-    rep = parity.compare_fast(oracle_lib, "hybrid", A, B, PARAM_SETS["bl"], got, dt)
+    # excused-tie budget ~2x the measured rate (fp64: 0 of 2^20, fp32: 0.29 %)
+    rep = parity.compare_fast(oracle_lib, "hybrid", A, B, PARAM_SETS["bl"], got, dt,
+                              max_excused=1e-4 if dt == np.float64 else 6e-3)
     assert rep["ok"], str(rep)
 
 
