@@ -6,7 +6,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-template <int M, int KIND>  // KIND 0: IADD3, 1: FFMA, 2: FSEL
+template <int M, int KIND>  // KIND 0: IADD3, 1: FFMA, 2: ISETP+SEL, 3: FSEL on a loop-invariant predicate, 4: predicated MOV
 __global__ void probe(double* out, int n) {
     double a[8];
     unsigned y[16];
@@ -15,6 +15,7 @@ __global__ void probe(double* out, int n) {
     for (int k = 0; k < 16; ++k) { y[k] = threadIdx.x + k; f[k] = threadIdx.x * 1e-3f + k; }
     const double b = 0.999999, c = 1e-7;
     for (int i = 0; i < n; ++i) {
+        const bool pr = ((y[0] >> 3) & 1u) != 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) a[k] = fma(a[k], b, c);
 #pragma unroll
@@ -22,6 +23,9 @@ __global__ void probe(double* out, int n) {
             if (KIND == 0) asm volatile("add.u32 %0, %0, %1;" : "+r"(y[k]) : "r"(k + 1));
             if (KIND == 1) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[k]) : "f"(0.999f), "f"(1e-3f));
             if (KIND == 2) asm volatile("{.reg .pred p; setp.lt.u32 p, %0, 100; selp.b32 %0, %0, %1, p;}" : "+r"(y[k]) : "r"(k));
+            // selects on a predicate computed once per iteration (one ISETP for all M)
+            if (KIND == 3) y[k] = pr ? y[k] + 1u : y[(k + 1) & 15];
+            if (KIND == 4) { if (pr) y[k] = y[(k + 3) & 15]; }
         }
     }
     double s = 0;
@@ -59,5 +63,10 @@ int main() {
     run<8, 1>("8 DFMA + 8 FFMA", d);
     run<16, 1>("8 DFMA + 16 FFMA", d);
     run<8, 2>("8 DFMA + 8 (ISETP+SEL)", d);
+    run<8, 3>("8 DFMA + 8 SEL", d);
+    run<16, 3>("8 DFMA + 16 SEL", d);
+    run<8, 4>("8 DFMA + 8 pred MOV", d);
+    run<16, 4>("8 DFMA + 16 pred MOV", d);
+    run<0, 3>("(no DFMA check) 8 DFMA", d);
     return 0;
 }
