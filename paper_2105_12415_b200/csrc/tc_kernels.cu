@@ -306,11 +306,11 @@ struct Tally {
     }
 
     // COMPARISON_IS_FALLBACK: hybrid comparisons also count as fallbacks
-    template <bool COMPARISON_IS_FALLBACK>
+    template <bool COMPARISON_IS_FALLBACK, int NWARPS = BLOCK / 32>
     __device__ void flush(tc_stats* s) {
         if (!s) return;
-        __shared__ unsigned long long red[5][BLOCK / 32];  // iterative, comparison, degenerate, contacts, intersecting
-        __shared__ double redm[BLOCK / 32];
+        __shared__ unsigned long long red[5][NWARPS];  // iterative, comparison, degenerate, contacts, intersecting
+        __shared__ double redm[NWARPS];
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
         unsigned long long it64 = iterative, cm64 = comparison, dg64 = degenerate, ct64 = contacts,
                            ix64 = intersecting;
@@ -756,6 +756,237 @@ __global__ void __launch_bounds__(BS_HYB, sizeof(T) == 4 ? TC_HYB_CTAS_F32 : TC_
     tl.flush<true>(a.stats);
 }
 
+
+// ---- warp-specialised hybrid (the fast fp64 hybrid) ----------------------------------
+// One CTA per SM.  WS_IW iterative warps stream their own 32-pair warp tiles
+// like iterative_kernel (no CTA barrier) and hand each open pair -- its index
+// AND its 18 coordinates, copied from the warp's stash -- to a shared-memory
+// ring; WS_FWG fallback warpgroups take batches of 128 from the ring and run
+// the degenerate screen and phase 1 on the ring slots in place, then move the
+// non-intersecting pairs (with their coordinates) to the warpgroup's phase-2
+// stack.  No queued pair is re-read from global memory, and the sweeps never
+// wait at a CTA barrier for the fallback.
+// TC_HYBRID_WS: 1 = this kernel for the fast fp64 hybrid (cfg1: 2.245 ->
+// 2.081 ms), 0 = the fused kernel everywhere.  TC_WS_IW_F32 > 0 would use it
+// for fp32 too (measured slower there: 12 + 8 warps 1.390 vs 1.375 ms fused,
+// the fp32 fallback being relatively heavier); strict builds keep the fused
+// kernel (strict fp64 +2.3 %).
+#ifndef TC_HYBRID_WS
+#define TC_HYBRID_WS 1
+#endif
+#ifndef TC_WS_IW_F64
+#define TC_WS_IW_F64 12
+#endif
+#ifndef TC_WS_IW_F32
+#define TC_WS_IW_F32 0
+#endif
+#ifndef TC_WS_FWG_F32
+#define TC_WS_FWG_F32 2
+#endif
+#ifndef TC_WS_RING
+#define TC_WS_RING 512
+#endif
+constexpr int WS_RING = TC_WS_RING;  // ring slots (256: 2.347 ms -- producers wait; 512-768: 2.08)
+constexpr int WS_FB = 128;           // threads of one fallback warpgroup (= one batch)
+constexpr int WS_Q2 = 2 * WS_FB;     // phase-2 stack entries per warpgroup
+static_assert((WS_RING & (WS_RING - 1)) == 0, "ring size");
+constexpr int64_t WS_FREE = -1;
+
+struct WsGroup {
+    int64_t q2[WS_Q2];  // pair index (| IDS_ONLY) of each phase-2 stack entry
+    int n2, m, pos;
+};
+template <int FWG>
+struct WsShared {
+    int64_t ring[WS_RING];  // pair index of each ring slot; WS_FREE = free
+    WsGroup g[FWG];
+    int tail, head, done;
+};
+// dynamic shared memory (T elements): [ring coordinates 18 x WS_RING]
+// [per warpgroup: phase-2 coordinates 18 x WS_Q2, crossing scratch SCR x WS_FB]
+// [iterative stash 18 x 32 IW]
+template <typename T, int IW, int FWG>
+constexpr size_t ws_smem_bytes() {
+    return sizeof(T) * (18 * WS_RING + FWG * (18 * WS_Q2 + SCR * WS_FB) + 18 * 32 * IW);
+}
+// named barrier of fallback warpgroup g (ids 1..FWG; 0 is __syncthreads)
+__device__ __forceinline__ void fb_sync(int g) { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(WS_FB) : "memory"); }
+
+template <typename T, bool STRICT, bool SOA, int WS_IW, int WS_FWG>
+__global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kernel(Args<T> a) {
+    using R = typename Pol<T, STRICT>::R;
+    constexpr int WS_IT = 32 * WS_IW;  // iterative threads
+    constexpr int WS_BS = WS_IT + WS_FWG * WS_FB;
+    __shared__ WsShared<WS_FWG> S;
+    extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
+    T* const ringd = reinterpret_cast<T*>(tc_dyn_smem);
+    Tally tl;
+    for (int k = threadIdx.x; k < WS_RING; k += WS_BS) S.ring[k] = WS_FREE;
+    if (threadIdx.x == 0) {
+        S.tail = S.head = S.done = 0;
+        for (int g = 0; g < WS_FWG; ++g) S.g[g].n2 = S.g[g].m = S.g[g].pos = 0;
+    }
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (wid < WS_IW) {
+        // ---- iterative warps ----
+        const KP<R> kp = make_kp<R>(a);
+        T* const slot = ringd + 18 * WS_RING + WS_FWG * (18 * WS_Q2 + SCR * WS_FB) + threadIdx.x;
+        const int64_t nwt = (a.n + 31) / 32;
+        for (int64_t wt = (int64_t)blockIdx.x * WS_IW + wid; wt < nwt; wt += (int64_t)gridDim.x * WS_IW) {
+            const int64_t i = wt * 32 + lane;
+            bool enq = false;
+            if (i < a.n) {
+                R A[9], B[9], eps;
+                load_pair<SOA>(a, i, A, B, eps);
+                stash_pair<WS_IT>(slot, A, B);
+                Rec<R> r;
+                run_iterative<WS_IT>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
+                tl.iterative++;
+                enq = r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i]);
+                store_rec<SOA>(a, i, r);  // open pairs: a placeholder the fallback overwrites
+                if (!enq) tl.result(r);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, enq);
+            if (m) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&S.tail, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (enq) {
+                    const int q = (base + __popc(m & ((1u << lane) - 1u))) & (WS_RING - 1);
+                    volatile int64_t* idx = &S.ring[q];
+                    while (*idx != WS_FREE) __nanosleep(64);  // ring full: the fallback frees slots
+                    __threadfence_block();  // the slot's previous reader is done before we overwrite it
+#pragma unroll
+                    for (int k = 0; k < 18; ++k) ringd[k * WS_RING + q] = slot[k * WS_IT];
+                    // the coordinates and the placeholder row before the index
+                    __threadfence_block();
+                    *idx = i;
+                }
+            }
+        }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) atomicAdd(&S.done, 1);
+    } else {
+        // ---- fallback warpgroups ----
+        const int gi = (threadIdx.x - WS_IT) / WS_FB, ft = (threadIdx.x - WS_IT) % WS_FB;
+        WsGroup& G = S.g[gi];
+        T* const q2d = ringd + 18 * WS_RING + gi * (18 * WS_Q2 + SCR * WS_FB);
+        Scratch<R> scr;
+        scr.p = q2d + 18 * WS_Q2 + ft;
+        scr.stride = WS_FB;
+        const bool want_ids = a.ids != nullptr;
+        const FlatSource<SOA, R, T, WS_FB> src{a, nullptr};  // (stores only)
+        auto phase2_batches = [&](bool final_) {
+            while (true) {
+                const int c2 = *(volatile int*)&G.n2;
+                fb_sync(gi);  // everyone has read the count before it changes
+                if (!(c2 >= WS_FB || (final_ && c2 > 0))) break;
+                const int m2 = c2 < WS_FB ? c2 : WS_FB;
+                const int sl = c2 - m2 + ft;
+                const int64_t e = ft < m2 ? G.q2[sl] : -1;
+                fb_sync(gi);
+                if (ft == 0) G.n2 = c2 - m2;
+                if (e >= 0) {
+                    const int64_t j = e & (IDS_ONLY - 1);
+                    const SmemTri<R> A{q2d + sl, WS_Q2}, B{q2d + 9 * WS_Q2 + sl, WS_Q2};
+                    const R eps = R(a.eps ? a.eps[j] : a.eps_scalar);
+                    Rec<R> r;
+                    const bool ids_only = (e & IDS_ONLY) != 0;
+                    comparison_phase2(A, B, eps, ids_only, r, scr);
+                    if (ids_only) {
+                        src.store_ids01(j, r.ids);
+                    } else {
+                        r.ids |= (uint32_t)FLAG_FALLBACK << 24;
+                        src.store(j, r);
+                        tl.result(r);
+                    }
+                }
+                fb_sync(gi);  // the stack slots are free again
+            }
+        };
+        while (true) {
+            if (ft == 0) {
+                // claim a batch of ring positions [h, h + m) for this warpgroup
+                int m = 0, h = 0;
+                while (true) {
+                    const int d = *(volatile int*)&S.done;
+                    __threadfence_block();
+                    h = *(volatile int*)&S.head;
+                    const int avail = *(volatile int*)&S.tail - h;
+                    m = avail >= WS_FB ? WS_FB : (d == WS_IW ? avail : 0);
+                    if (m > 0) {
+                        if (atomicCAS(&S.head, h, h + m) == h) break;
+                        continue;
+                    }
+                    if (d == WS_IW) break;  // all produced and claimed
+                    __nanosleep(256);
+                }
+                G.m = m;
+                G.pos = h;
+            }
+            fb_sync(gi);
+            const int m = *(volatile int*)&G.m, pos = *(volatile int*)&G.pos;
+            if (m == 0) break;
+            const int q = (pos + ft) & (WS_RING - 1);
+            int64_t j = -1;
+            if (ft < m) {
+                volatile int64_t* idx = &S.ring[q];
+                while ((j = *idx) == WS_FREE) __nanosleep(32);  // claimed by a producer, not yet written
+                __threadfence_block();
+            }
+            bool push2 = false;
+            int64_t e2 = 0;
+            if (j >= 0) {
+                const SmemTri<R> A{ringd + q, WS_RING}, B{ringd + 9 * WS_RING + q, WS_RING};
+                const R eps = R(a.eps ? a.eps[j] : a.eps_scalar);
+                Rec<R> r;
+                // RK/kernels.py:596-600: a degenerate open pair keeps its
+                // iterative result and is marked DEGENERATE
+                if (degenerate_tri_t<R>(A) || degenerate_tri_t<R>(B)) {
+                    src.mark_degenerate(j);
+                    tl.degenerate++;
+                } else {
+                    tl.comparison++;
+                    if (comparison_phase1(A, B, eps, scr, r)) {
+                        r.ids |= (uint32_t)FLAG_FALLBACK << 24;
+                        src.store(j, r);
+                        tl.result(r);
+                        push2 = want_ids;
+                        e2 = j | IDS_ONLY;
+                    } else {
+                        push2 = true;
+                        e2 = j;
+                    }
+                }
+            }
+            // move phase-2 pairs (index and coordinates) to the stack, then free the ring slots
+            {
+                const unsigned mm = __ballot_sync(0xffffffffu, push2);
+                int base = 0;
+                if (mm) {
+                    if ((ft & 31) == 0) base = atomicAdd(&G.n2, __popc(mm));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                }
+                if (push2) {
+                    const int sl = base + __popc(mm & ((1u << (ft & 31)) - 1u));
+                    TC_CHECK(sl < WS_Q2);
+                    G.q2[sl] = e2;
+#pragma unroll
+                    for (int k = 0; k < 18; ++k) q2d[k * WS_Q2 + sl] = ringd[k * WS_RING + q];
+                }
+            }
+            // every read of the ring slot (phase 1, the copy) before it is freed
+            __threadfence_block();
+            if (ft < m) *(volatile int64_t*)&S.ring[q] = WS_FREE;
+            fb_sync(gi);  // q2 entries visible, G.m / G.pos read by everyone
+            phase2_batches(false);
+        }
+        phase2_batches(true);
+    }
+    tl.flush<true, WS_BS / 32>(a.stats);
+}
 
 // ---- all-pairs particle-block kernel (BASELINE.json config 2) -----------------
 // One CTA per particle-pair block at a time (grid-stride over blocks): both
@@ -1339,6 +1570,18 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         auto k = iterative_kernel<T, STRICT, SOA>;
         const size_t smem = sizeof(T) * 2 * SLOT * BS_ITER;  // double-buffered pair slots
         k<<<(unsigned)grid_for(k, a.n, smem, BS_ITER), BS_ITER, smem, s>>>(a);
+    } else if constexpr (TC_HYBRID_WS && !STRICT && (sizeof(T) == 8 ? TC_WS_IW_F64 : TC_WS_IW_F32) > 0) {
+        // warp-specialised hybrid: one CTA per SM
+        constexpr int IW = sizeof(T) == 8 ? TC_WS_IW_F64 : (TC_WS_IW_F32 > 0 ? TC_WS_IW_F32 : 1);
+        constexpr int FWG = sizeof(T) == 8 ? 1 : TC_WS_FWG_F32;
+        auto k = hybrid_ws_kernel<T, STRICT, SOA, IW, FWG>;
+        const size_t smem = ws_smem_bytes<T, IW, FWG>();
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t ctas = (a.n + 32 * IW - 1) / (32 * IW);
+        int64_t g = ctas < sm_count() ? ctas : sm_count();
+        const int64_t cap = g_max_ctas.load(std::memory_order_relaxed);  // test knob
+        if (cap > 0 && g > cap) g = cap;
+        k<<<(unsigned)g, 32 * IW + FWG * WS_FB, smem, s>>>(a);
     } else {
         auto k = hybrid_kernel<T, STRICT, SOA>;
 #ifndef TC_X_PAD
