@@ -49,8 +49,12 @@ for r in range(args.rounds):
         call = (lambda: fn(ptr(ta), ptr(tb), n, None, allow, ctypes.byref(p), *cols, None, ptr(stats), None)) \
             if args.variant == "hybrid" else \
             (lambda: fn(ptr(ta), ptr(tb), n, None, ctypes.byref(p), *cols, None, ptr(stats), None))
-        for _ in range(2):
-            assert call() == 0
+        rc = [call() for _ in range(2)]
+        if any(rc):
+            print(f"{name}: launch failed rc={rc} ({lib.tc_last_error().decode() if hasattr(lib, 'tc_last_error') else ''})",
+                  flush=True)
+            res[name].append(float('nan'))
+            continue
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         lib.tc_stats_reset(ptr(stats), None)
         e0.record()
@@ -61,6 +65,6 @@ for r in range(args.rounds):
         res[name].append(e0.elapsed_time(e1) / args.reps)
         stats_of[name] = D.read_stats(stats)
 for name, ts in res.items():
-    st = stats_of[name]
+    st = stats_of.get(name, {"fallback": 0, "contacts": 0})
     print(f"{name:40s} {min(ts):7.3f} ms  {n / min(ts) / 1e6:8.1f} M pairs/s  (rounds {' '.join(f'{t:.3f}' for t in ts)})"
           f"  fb {st['fallback'] // (args.reps + 0)} contacts {st['contacts'] // args.reps}", flush=True)
