@@ -364,7 +364,9 @@ def main():
         "bound": "fp64", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
         "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
         "traffic_source": traffic_note, "algorithmic_bytes_per_launch": n * bytes_per_pair,
-        "kernel": f"hybrid_kernel<double,{'strict' if args.strict else 'fast'},soa>", "kernel_ms": ms_kernel,
+        "kernel": ("hybrid_kernel<double,strict,soa>" if args.strict else
+                   "hybrid_ws_kernel<double,fast,soa,12,1> (warp-specialised: 12 iterative + 4 fallback warps per SM)"),
+        "kernel_ms": ms_kernel,
         "flops_per_launch": flops,
         "flop_model": "SURVEY.md 8(d)/App. A algorithmic work: n(200+88N) + 1199 fallback + 254 fallback&intersect "
                       "(N = 16 sweeps; fallback and intersect counts from this run's tc_stats)",

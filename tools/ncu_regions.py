@@ -43,6 +43,7 @@ REGIONS = [
     ("tally", "tc_kernels.cu", r"struct Tally"),
     ("prefetch", "tc_kernels.cu", r"void prefetch_tile\("),
     ("drain", "tc_kernels.cu", r"void drain\(const Src& src"),
+    ("ws_kernel_body", "tc_kernels.cu", r"hybrid_ws_kernel\(Args<T> a\)"),
 ]
 
 
@@ -118,8 +119,11 @@ def main():
     lib = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "paper_2105_12415_b200", "libtricontact_b200.so")
     sp = spans()
     chains = line_chains(lib, mangled)
-    ksub = {"hybrid_kernelIdLb0ELb1": "hybrid_kernel<double, (bool)0, (bool)1>",
-            "hybrid_kernelIfLb0ELb1": "hybrid_kernel<float, (bool)0, (bool)1>"}.get(mangled, mangled)
+    m = re.match(r"(\w+?)I([df])Lb([01])ELb([01])E?(?:Li(\d+)ELi(\d+)E)?", mangled)
+    ksub = mangled
+    if m:
+        ksub = f"{m.group(1)}<{'double' if m.group(2) == 'd' else 'float'}, (bool){m.group(3)}, (bool){m.group(4)}"
+        ksub += f", {m.group(5)}, {m.group(6)}>" if m.group(5) else ">"
     rows = sass_rows(rep, ksub)
     base = min(a for a, *_ in rows)
     agg = collections.defaultdict(lambda: collections.Counter())
