@@ -123,7 +123,7 @@ def main():
     ksub = mangled
     if m:
         ksub = f"{m.group(1)}<{'double' if m.group(2) == 'd' else 'float'}, (bool){m.group(3)}, (bool){m.group(4)}"
-        ksub += f", {m.group(5)}, {m.group(6)}>" if m.group(5) else ">"
+        ksub += f", (int){m.group(5)}, (int){m.group(6)}>" if m.group(5) else ">"
     rows = sass_rows(rep, ksub)
     base = min(a for a, *_ in rows)
     agg = collections.defaultdict(lambda: collections.Counter())
