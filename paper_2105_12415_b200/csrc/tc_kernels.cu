@@ -766,11 +766,12 @@ __global__ void __launch_bounds__(BS_HYB, sizeof(T) == 4 ? TC_HYB_CTAS_F32 : TC_
 // non-intersecting pairs (with their coordinates) to the warpgroup's phase-2
 // stack.  No queued pair is re-read from global memory, and the sweeps never
 // wait at a CTA barrier for the fallback.
-// TC_HYBRID_WS: 1 = this kernel for the fast fp64 hybrid (cfg1: 2.245 ->
-// 2.081 ms), 0 = the fused kernel everywhere.  TC_WS_IW_F32 > 0 would use it
-// for fp32 too (measured slower there: 12 + 8 warps 1.390 vs 1.375 ms fused,
-// the fp32 fallback being relatively heavier); strict builds keep the fused
-// kernel (strict fp64 +2.3 %).
+// TC_HYBRID_WS: 1 = this kernel for the fast hybrids, 0 = the fused kernel
+// everywhere.  fp64: 12 iterative warps + 1 fallback warpgroup at 128
+// registers (cfg1 2.245 -> 2.081 ms; 10 + 4 and 8 + 8 measured slower);
+// fp32 (80 registers): 16 + 8 warps (1.375 -> 1.290 ms; 12 + 8 1.390, 18 + 8
+// 1.325, 16 + 12 1.312).  Strict builds keep the fused kernel (with this one:
+// fp64 +3.3 %, fp32 +8.3 %; TC_WS_STRICT).
 #ifndef TC_HYBRID_WS
 #define TC_HYBRID_WS 1
 #endif
@@ -778,10 +779,13 @@ __global__ void __launch_bounds__(BS_HYB, sizeof(T) == 4 ? TC_HYB_CTAS_F32 : TC_
 #define TC_WS_IW_F64 12
 #endif
 #ifndef TC_WS_IW_F32
-#define TC_WS_IW_F32 0
+#define TC_WS_IW_F32 16
 #endif
 #ifndef TC_WS_FWG_F32
 #define TC_WS_FWG_F32 2
+#endif
+#ifndef TC_WS_STRICT
+#define TC_WS_STRICT 0
 #endif
 #ifndef TC_WS_RING
 #define TC_WS_RING 512
@@ -1570,7 +1574,7 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         auto k = iterative_kernel<T, STRICT, SOA>;
         const size_t smem = sizeof(T) * 2 * SLOT * BS_ITER;  // double-buffered pair slots
         k<<<(unsigned)grid_for(k, a.n, smem, BS_ITER), BS_ITER, smem, s>>>(a);
-    } else if constexpr (TC_HYBRID_WS && !STRICT && (sizeof(T) == 8 ? TC_WS_IW_F64 : TC_WS_IW_F32) > 0) {
+    } else if constexpr (TC_HYBRID_WS && (!STRICT || TC_WS_STRICT) && (sizeof(T) == 8 ? TC_WS_IW_F64 : TC_WS_IW_F32) > 0) {
         // warp-specialised hybrid: one CTA per SM
         constexpr int IW = sizeof(T) == 8 ? TC_WS_IW_F64 : (TC_WS_IW_F32 > 0 ? TC_WS_IW_F32 : 1);
         constexpr int FWG = sizeof(T) == 8 ? 1 : TC_WS_FWG_F32;
