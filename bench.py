@@ -786,7 +786,7 @@ def roofline_f32(D, torch, lib, ta, tb, n, dev, stream, reps=5):
     flops = flops_reference_model(n, PARAMS["n_iterative"], s["fallback"], s["intersecting"])
     peak = fma_peak(torch, lib, stream, dev, fp64=False)
     achieved = flops / (ms / 1e3) / 1e12
-    return {"bound": "fp32", "kernel": "hybrid_kernel<float,fast,soa>", "achieved": achieved, "peak": peak,
+    return {"bound": "fp32", "kernel": "hybrid_ws_kernel<float,fast,soa,16,2> (warp-specialised: 16 iterative + 8 fallback warps per SM)", "achieved": achieved, "peak": peak,
             "unit": "TFLOP/s", "frac": achieved / peak, "kernel_ms": ms, "pairs_per_s": n / (ms / 1e3),
             "fallback_rate": s["fallback"] / n, "flops_per_launch": flops,
             "flop_model": "SURVEY.md 8(d)/App. A, as roofline", "peak_source": "in-run FFMA probe (tc_fma_probe)",
