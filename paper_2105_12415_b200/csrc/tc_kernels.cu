@@ -781,6 +781,9 @@ __global__ void __launch_bounds__(BS_HYB, sizeof(T) == 4 ? TC_HYB_CTAS_F32 : TC_
 #ifndef TC_WS_IW_F32
 #define TC_WS_IW_F32 16
 #endif
+#ifndef TC_WS_FWG_F64
+#define TC_WS_FWG_F64 1
+#endif
 #ifndef TC_WS_FWG_F32
 #define TC_WS_FWG_F32 2
 #endif
@@ -790,10 +793,26 @@ __global__ void __launch_bounds__(BS_HYB, sizeof(T) == 4 ? TC_HYB_CTAS_F32 : TC_
 #ifndef TC_WS_RING
 #define TC_WS_RING 512
 #endif
+// TC_WS_ASYNC: each iterative warp double-buffers its 32-pair stash and pulls
+// its next tile into the spare buffer with 16-byte cp.async.cg copies (no
+// registers, L1 bypassed) while the current tile computes.
+#ifndef TC_WS_IT_REGS
+#define TC_WS_IT_REGS 0
+#endif
+#ifndef TC_WS_FB_REGS
+#define TC_WS_FB_REGS 0
+#endif
+#ifndef TC_WS_ASYNC
+#define TC_WS_ASYNC 0
+#endif
+#ifndef TC_WS_Q2
+#define TC_WS_Q2 256
+#endif
 constexpr int WS_RING = TC_WS_RING;  // ring slots (256: 2.347 ms -- producers wait; 512-768: 2.08)
 constexpr int WS_FB = 128;           // threads of one fallback warpgroup (= one batch)
-constexpr int WS_Q2 = 2 * WS_FB;     // phase-2 stack entries per warpgroup
-static_assert((WS_RING & (WS_RING - 1)) == 0, "ring size");
+constexpr int WS_Q2 = TC_WS_Q2;      // phase-2 stack entries per warpgroup (< 2 WS_FB: phase-1 batches shrink to fit)
+constexpr int WS_NBUF = TC_WS_ASYNC ? 2 : 1;  // stash buffers per iterative warp
+static_assert(WS_Q2 >= WS_FB + 32 && WS_Q2 <= 2 * WS_FB, "phase-2 stack size");
 constexpr int64_t WS_FREE = -1;
 
 struct WsGroup {
@@ -811,7 +830,7 @@ struct WsShared {
 // [iterative stash 18 x 32 IW]
 template <typename T, int IW, int FWG>
 constexpr size_t ws_smem_bytes() {
-    return sizeof(T) * (18 * WS_RING + FWG * (18 * WS_Q2 + SCR * WS_FB) + 18 * 32 * IW);
+    return sizeof(T) * (18 * WS_RING + FWG * (18 * WS_Q2 + SCR * WS_FB) + WS_NBUF * 18 * 32 * IW);
 }
 // named barrier of fallback warpgroup g (ids 1..FWG; 0 is __syncthreads)
 __device__ __forceinline__ void fb_sync(int g) { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(WS_FB) : "memory"); }
@@ -834,18 +853,61 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (wid < WS_IW) {
         // ---- iterative warps ----
+        if constexpr (TC_WS_FB_REGS > 0 && TC_WS_IT_REGS > 0 && sizeof(T) == 8)
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(TC_WS_IT_REGS));
         const KP<R> kp = make_kp<R>(a);
-        T* const slot = ringd + 18 * WS_RING + WS_FWG * (18 * WS_Q2 + SCR * WS_FB) + threadIdx.x;
+        // the warp's stash: WS_NBUF buffers of [18][32] values
+        T* const wstash = ringd + 18 * WS_RING + WS_FWG * (18 * WS_Q2 + SCR * WS_FB) + wid * (WS_NBUF * 18 * 32);
         const int64_t nwt = (a.n + 31) / 32;
-        for (int64_t wt = (int64_t)blockIdx.x * WS_IW + wid; wt < nwt; wt += (int64_t)gridDim.x * WS_IW) {
+        const int64_t wstep = (int64_t)gridDim.x * WS_IW;
+        // 16-byte copies need every SoA plane row 16-byte aligned
+        constexpr int CH = 16 / (int)sizeof(T);  // values per copy
+        const bool can_async = TC_WS_ASYNC && SOA && a.n % CH == 0 &&
+                               ((reinterpret_cast<uintptr_t>(a.tri_a) | reinterpret_cast<uintptr_t>(a.tri_b)) & 15) == 0;
+        auto pre = [&](int64_t wt) { return can_async && wt < nwt && (wt + 1) * 32 <= a.n; };  // full tiles only
+        auto issue = [&](int64_t wt, T* buf) {
+            constexpr int LPP = 32 / CH;   // lanes per plane row
+            constexpr int PPI = 32 / LPP;  // plane rows per instruction
+            const int pl = lane / LPP, off = (lane % LPP) * CH;
+#pragma unroll
+            for (int j = 0; j < (18 + PPI - 1) / PPI; ++j) {
+                const int k = j * PPI + pl;
+                if (k < 18) {
+                    const T* src = (k < 9 ? a.tri_a + (int64_t)k * a.n : a.tri_b + (int64_t)(k - 9) * a.n) + wt * 32 + off;
+                    const unsigned d = (unsigned)__cvta_generic_to_shared(buf + k * 32 + off);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        int cur = 0;
+        const int64_t wt0 = (int64_t)blockIdx.x * WS_IW + wid;
+        if (pre(wt0)) issue(wt0, wstash);
+        for (int64_t wt = wt0; wt < nwt; wt += wstep) {
             const int64_t i = wt * 32 + lane;
+            T* const slot = wstash + cur * (18 * 32) + lane;
+            const bool staged = pre(wt);
+            if (TC_WS_ASYNC) {
+                if (staged) cp_async_wait_all();
+                __syncwarp();  // the tile is visible to every lane; the previous tile's reads of the spare buffer are done
+                cur ^= 1;
+                if (pre(wt + wstep)) issue(wt + wstep, wstash + cur * (18 * 32));
+            }
             bool enq = false;
             if (i < a.n) {
                 R A[9], B[9], eps;
-                load_pair<SOA>(a, i, A, B, eps);
-                stash_pair<WS_IT>(slot, A, B);
+                if (staged) {
+#pragma unroll
+                    for (int k = 0; k < 9; ++k) {
+                        A[k] = R(slot[k * 32]);
+                        B[k] = R(slot[(9 + k) * 32]);
+                    }
+                } else {
+                    load_pair<SOA>(a, i, A, B, eps);
+                    stash_pair<32>(slot, A, B);
+                }
                 Rec<R> r;
-                run_iterative<WS_IT>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
+                run_iterative<32>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
                 tl.iterative++;
                 enq = r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i]);
                 store_rec<SOA>(a, i, r);  // open pairs: a placeholder the fallback overwrites
@@ -857,12 +919,12 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
                 if (lane == 0) base = atomicAdd(&S.tail, __popc(m));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 if (enq) {
-                    const int q = (base + __popc(m & ((1u << lane) - 1u))) & (WS_RING - 1);
+                    const int q = (unsigned)(base + __popc(m & ((1u << lane) - 1u))) % (unsigned)WS_RING;
                     volatile int64_t* idx = &S.ring[q];
                     while (*idx != WS_FREE) __nanosleep(64);  // ring full: the fallback frees slots
                     __threadfence_block();  // the slot's previous reader is done before we overwrite it
 #pragma unroll
-                    for (int k = 0; k < 18; ++k) ringd[k * WS_RING + q] = slot[k * WS_IT];
+                    for (int k = 0; k < 18; ++k) ringd[k * WS_RING + q] = slot[k * 32];
                     // the coordinates and the placeholder row before the index
                     __threadfence_block();
                     *idx = i;
@@ -874,6 +936,13 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
         if (lane == 0) atomicAdd(&S.done, 1);
     } else {
         // ---- fallback warpgroups ----
+        // TC_WS_FB_REGS: the launch allocates 65536 / threads registers per
+        // thread (96 at 640 threads); the fallback warpgroups take the spare
+        // ones (setmaxnreg needs warpgroup-aligned roles: WS_IW % 4 == 0)
+        if constexpr (TC_WS_FB_REGS > 0 && sizeof(T) == 8) {
+            static_assert(WS_IW % 4 == 0, "setmaxnreg is per warpgroup");
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(TC_WS_FB_REGS));
+        }
         const int gi = (threadIdx.x - WS_IT) / WS_FB, ft = (threadIdx.x - WS_IT) % WS_FB;
         WsGroup& G = S.g[gi];
         T* const q2d = ringd + 18 * WS_RING + gi * (18 * WS_Q2 + SCR * WS_FB);
@@ -919,7 +988,9 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
                     __threadfence_block();
                     h = *(volatile int*)&S.head;
                     const int avail = *(volatile int*)&S.tail - h;
-                    m = avail >= WS_FB ? WS_FB : (d == WS_IW ? avail : 0);
+                    // a batch must fit the phase-2 stack (n2 < WS_FB here)
+                    const int want = WS_Q2 < 2 * WS_FB ? min(WS_FB, WS_Q2 - *(volatile int*)&G.n2) : WS_FB;
+                    m = avail >= want ? want : (d == WS_IW ? avail : 0);
                     if (m > 0) {
                         if (atomicCAS(&S.head, h, h + m) == h) break;
                         continue;
@@ -933,7 +1004,7 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
             fb_sync(gi);
             const int m = *(volatile int*)&G.m, pos = *(volatile int*)&G.pos;
             if (m == 0) break;
-            const int q = (pos + ft) & (WS_RING - 1);
+            const int q = (unsigned)(pos + ft) % (unsigned)WS_RING;
             int64_t j = -1;
             if (ft < m) {
                 volatile int64_t* idx = &S.ring[q];
@@ -990,6 +1061,206 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
         phase2_batches(true);
     }
     tl.flush<true, WS_BS / 32>(a.stats);
+}
+
+// ---- warp-specialised hybrid, warp-granular fallback (TC_WSW) ---------------------------
+// The same ring hand-over as hybrid_ws_kernel, but every fallback warp works
+// on its own: it claims 32 ring slots at a time, runs the degenerate screen
+// and phase 1 on them in place, moves the non-intersecting pairs to its own
+// 64-entry phase-2 stack and runs phase-2 batches of 32 -- no named barriers,
+// no shared batch state, and any number of fallback warps (WSW_FW), so the
+// CTA need not be 16 warps: the ncu line counts of the 12 + 4 kernel showed
+// its iterative warps asleep on a full ring ~17 x 64 ns per tile, i.e. four
+// fallback warps (one per SM sub-partition, latency-bound at one instruction
+// per ~7 cycles) set the pace.
+#ifndef TC_WSW
+#define TC_WSW 0
+#endif
+#ifndef TC_WSW_IW
+#define TC_WSW_IW 12
+#endif
+#ifndef TC_WSW_FW
+#define TC_WSW_FW 6
+#endif
+constexpr int WSW_Q2 = 64;  // phase-2 stack entries per fallback warp
+template <typename T, int IW, int FW>
+constexpr size_t wsw_smem_bytes() {
+    return sizeof(T) * (18 * WS_RING + FW * (18 * WSW_Q2 + SCR * 32) + 18 * 32 * IW);
+}
+template <int FW>
+struct WswShared {
+    int64_t ring[WS_RING];  // pair index of each ring slot
+    // Slot sequence numbers (bounded multi-producer / multi-consumer queue):
+    // slot q starts at q; the producer holding position p waits for
+    // seq == p, fills the slot and sets p + 1; the consumer holding p waits for
+    // p + 1, reads and sets p + WS_RING (free for the next lap).  Several
+    // consumers can therefore hold claims a lap apart without mistaking the
+    // previous lap's entry for theirs.
+    int seq[WS_RING];
+    int64_t q2[FW][WSW_Q2];
+    int tail, head, done;
+};
+
+template <typename T, bool STRICT, bool SOA, int IW, int FW>
+__global__ void __launch_bounds__(32 * (IW + FW), 1) hybrid_wsw_kernel(Args<T> a) {
+    using R = typename Pol<T, STRICT>::R;
+    constexpr int NT = 32 * (IW + FW);
+    __shared__ WswShared<FW> S;
+    extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
+    T* const ringd = reinterpret_cast<T*>(tc_dyn_smem);
+    Tally tl;
+    for (int k = threadIdx.x; k < WS_RING; k += NT) S.seq[k] = k;
+    if (threadIdx.x == 0) S.tail = S.head = S.done = 0;
+    __syncthreads();
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (wid < IW) {
+        // ---- iterative warps (as in hybrid_ws_kernel) ----
+        const KP<R> kp = make_kp<R>(a);
+        T* const slot = ringd + 18 * WS_RING + FW * (18 * WSW_Q2 + SCR * 32) + wid * (18 * 32) + lane;
+        const int64_t nwt = (a.n + 31) / 32;
+        for (int64_t wt = (int64_t)blockIdx.x * IW + wid; wt < nwt; wt += (int64_t)gridDim.x * IW) {
+            const int64_t i = wt * 32 + lane;
+            bool enq = false;
+            if (i < a.n) {
+                R A[9], B[9], eps;
+                load_pair<SOA>(a, i, A, B, eps);
+                stash_pair<32>(slot, A, B);
+                Rec<R> r;
+                run_iterative<32>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
+                tl.iterative++;
+                enq = r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i]);
+                store_rec<SOA>(a, i, r);  // open pairs: a placeholder the fallback overwrites
+                if (!enq) tl.result(r);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, enq);
+            if (m) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&S.tail, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (enq) {
+                    const int pos = base + __popc(m & ((1u << lane) - 1u));
+                    const int q = (unsigned)pos % (unsigned)WS_RING;
+                    volatile int* sq = &S.seq[q];
+                    while (*sq != pos) __nanosleep(64);  // ring full: the fallback frees slots
+                    __threadfence_block();  // the slot's previous reader is done before we overwrite it
+#pragma unroll
+                    for (int k = 0; k < 18; ++k) ringd[k * WS_RING + q] = slot[k * 32];
+                    S.ring[q] = i;
+                    __threadfence_block();  // the slot and the placeholder row before the sequence number
+                    *sq = pos + 1;
+                }
+            }
+        }
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) atomicAdd(&S.done, 1);
+    } else {
+        // ---- fallback warps ----
+        const int fw = wid - IW;
+        T* const q2d = ringd + 18 * WS_RING + fw * (18 * WSW_Q2 + SCR * 32);
+        int64_t* const q2i = S.q2[fw];
+        Scratch<R> scr;
+        scr.p = q2d + 18 * WSW_Q2 + lane;
+        scr.stride = 32;
+        const bool want_ids = a.ids != nullptr;
+        const FlatSource<SOA, R, T, 32> src{a, nullptr};  // (stores only)
+        int n2 = 0;  // entries on this warp's phase-2 stack (warp-uniform)
+        auto phase2_batches = [&](bool final_) {
+            while (n2 >= 32 || (final_ && n2 > 0)) {
+                const int m2 = n2 < 32 ? n2 : 32;
+                const int sl = n2 - m2 + lane;
+                n2 -= m2;
+                if (lane < m2) {
+                    const int64_t e = q2i[sl];
+                    const int64_t j = e & (IDS_ONLY - 1);
+                    const SmemTri<R> A{q2d + sl, WSW_Q2}, B{q2d + 9 * WSW_Q2 + sl, WSW_Q2};
+                    const R eps = R(a.eps ? a.eps[j] : a.eps_scalar);
+                    Rec<R> r;
+                    const bool ids_only = (e & IDS_ONLY) != 0;
+                    comparison_phase2(A, B, eps, ids_only, r, scr);
+                    if (ids_only) {
+                        src.store_ids01(j, r.ids);
+                    } else {
+                        r.ids |= (uint32_t)FLAG_FALLBACK << 24;
+                        src.store(j, r);
+                        tl.result(r);
+                    }
+                }
+                __syncwarp();  // the stack slots are free again
+            }
+        };
+        while (true) {
+            int m = 0, h = 0;
+            if (lane == 0) {
+                // claim ring positions [h, h + m) for this warp
+                while (true) {
+                    const int d = *(volatile int*)&S.done;
+                    __threadfence_block();
+                    h = *(volatile int*)&S.head;
+                    const int avail = *(volatile int*)&S.tail - h;
+                    m = avail >= 32 ? 32 : (d == IW ? avail : 0);
+                    if (m > 0) {
+                        if (atomicCAS(&S.head, h, h + m) == h) break;
+                        continue;
+                    }
+                    if (d == IW) break;  // all produced and claimed
+                    __nanosleep(128);
+                }
+            }
+            m = __shfl_sync(0xffffffffu, m, 0);
+            h = __shfl_sync(0xffffffffu, h, 0);
+            if (m == 0) break;
+            const int q = (unsigned)(h + lane) % (unsigned)WS_RING;
+            int64_t j = -1;
+            if (lane < m) {
+                volatile int* sq = &S.seq[q];
+                while (*sq != h + lane + 1) __nanosleep(32);  // claimed by a producer, not yet written
+                __threadfence_block();
+                j = *(volatile int64_t*)&S.ring[q];
+            }
+            bool push2 = false;
+            int64_t e2 = 0;
+            if (j >= 0) {
+                const SmemTri<R> A{ringd + q, WS_RING}, B{ringd + 9 * WS_RING + q, WS_RING};
+                const R eps = R(a.eps ? a.eps[j] : a.eps_scalar);
+                Rec<R> r;
+                // RK/kernels.py:596-600: a degenerate open pair keeps its
+                // iterative result and is marked DEGENERATE
+                if (degenerate_tri_t<R>(A) || degenerate_tri_t<R>(B)) {
+                    src.mark_degenerate(j);
+                    tl.degenerate++;
+                } else {
+                    tl.comparison++;
+                    if (comparison_phase1(A, B, eps, scr, r)) {
+                        r.ids |= (uint32_t)FLAG_FALLBACK << 24;
+                        src.store(j, r);
+                        tl.result(r);
+                        push2 = want_ids;
+                        e2 = j | IDS_ONLY;
+                    } else {
+                        push2 = true;
+                        e2 = j;
+                    }
+                }
+            }
+            // move phase-2 pairs (index and coordinates) to the warp's stack, then free the ring slots
+            const unsigned mm = __ballot_sync(0xffffffffu, push2);
+            if (push2) {
+                const int sl = n2 + __popc(mm & ((1u << lane) - 1u));
+                TC_CHECK(sl < WSW_Q2);
+                q2i[sl] = e2;
+#pragma unroll
+                for (int k = 0; k < 18; ++k) q2d[k * WSW_Q2 + sl] = ringd[k * WS_RING + q];
+            }
+            n2 += __popc(mm);
+            __threadfence_block();  // every read of the ring slot (phase 1, the copy) before it is freed
+            if (lane < m) *(volatile int*)&S.seq[q] = h + lane + WS_RING;
+            __syncwarp();
+            phase2_batches(false);
+        }
+        phase2_batches(true);
+    }
+    tl.flush<true, NT / 32>(a.stats);
 }
 
 // ---- all-pairs particle-block kernel (BASELINE.json config 2) -----------------
@@ -1574,10 +1845,21 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         auto k = iterative_kernel<T, STRICT, SOA>;
         const size_t smem = sizeof(T) * 2 * SLOT * BS_ITER;  // double-buffered pair slots
         k<<<(unsigned)grid_for(k, a.n, smem, BS_ITER), BS_ITER, smem, s>>>(a);
+    } else if constexpr (TC_WSW && !STRICT && sizeof(T) == 8) {
+        // warp-specialised hybrid with warp-granular fallback: one CTA per SM
+        constexpr int IW = TC_WSW_IW, FW = TC_WSW_FW;
+        auto k = hybrid_wsw_kernel<T, STRICT, SOA, IW, FW>;
+        const size_t smem = wsw_smem_bytes<T, IW, FW>();
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int64_t ctas = (a.n + 32 * IW - 1) / (32 * IW);
+        int64_t g = ctas < sm_count() ? ctas : sm_count();
+        const int64_t cap = g_max_ctas.load(std::memory_order_relaxed);  // test knob
+        if (cap > 0 && g > cap) g = cap;
+        k<<<(unsigned)g, 32 * (IW + FW), smem, s>>>(a);
     } else if constexpr (TC_HYBRID_WS && (!STRICT || TC_WS_STRICT) && (sizeof(T) == 8 ? TC_WS_IW_F64 : TC_WS_IW_F32) > 0) {
         // warp-specialised hybrid: one CTA per SM
         constexpr int IW = sizeof(T) == 8 ? TC_WS_IW_F64 : (TC_WS_IW_F32 > 0 ? TC_WS_IW_F32 : 1);
-        constexpr int FWG = sizeof(T) == 8 ? 1 : TC_WS_FWG_F32;
+        constexpr int FWG = sizeof(T) == 8 ? TC_WS_FWG_F64 : TC_WS_FWG_F32;
         auto k = hybrid_ws_kernel<T, STRICT, SOA, IW, FWG>;
         const size_t smem = ws_smem_bytes<T, IW, FWG>();
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -741,13 +741,25 @@ __device__ __forceinline__ Strict<T> clip0_hi(Strict<T> x, Strict<T> hi) { retur
 // every later use rounds away), then the upper clip's compare and select:
 // 5 issue slots instead of 7 (tools/sweep_probe2.cu: 147 -> 142 cycles per
 // warp-sweep).  Not bitwise: strict mode keeps clip0_hi.
+#ifndef TC_UPCLIP_INT
+#define TC_UPCLIP_INT 0
+#endif
+#ifndef TC_SLIDE_ONE
+#define TC_SLIDE_ONE 0
+#endif
 #ifndef TC_LOWCLIP_IMNMX
 #define TC_LOWCLIP_IMNMX 1
 #endif
 __device__ __forceinline__ double clip0_hi_fast(double x, double hi) {
 #if TC_LOWCLIP_IMNMX
     const double m = __hiloint2double(max(__double2hiint(x), 0), __double2loint(x));
+#if TC_UPCLIP_INT
+    // m >= 0: the IEEE order is the unsigned order of the bit patterns (a hi
+    // below 0 by an ulp keeps m); two integer compares instead of a DSETP
+    return ((unsigned long long)__double_as_longlong(m) < (unsigned long long)__double_as_longlong(hi)) ? m : hi;
+#else
     return (m < hi) ? m : hi;
+#endif
 #else
     return clip0_hi(x, hi);
 #endif
@@ -972,6 +984,20 @@ struct GramSolver {
     // the box, so the inner max() of the clips are identities (coord_step)
     __device__ __forceinline__ R hi_of(R xp) const { return BOX ? R(1) - xp : maxv(R(0), R(1) - maxv(xp, R(0))); }
 
+    // Box-mode slide as ONE one-sided clip (TC_SLIDE_ONE): the slide moves
+    // x_a by -t and x_b by +t with t in [-x_b, x_a], i.e. x_a's target
+    // x_a + q (q = (g_b - g_a) r, the negated unclipped t) is clipped to
+    // [0, x_a + x_b] and x_b takes the rest of the sum: one lower clip on the
+    // integer pipe and one compare instead of two compares and four selects.
+    // s = the step of x_a (= -t); the caller updates g by -s * S_k.
+    __device__ __forceinline__ static void slide_one(R& xa, R& xb, R q, R& s) {
+        const R h = xa + xb;
+        const R t = clip0_hi_fast(xa + q, h);
+        s = t - xa;
+        xa = t;
+        xb = h - t;
+    }
+
     __device__ __forceinline__ void sweep() {
         R t, s;
         t = clip0_hi_fast(x0 - g0 * r0, hi_of(x1));
@@ -980,20 +1006,30 @@ struct GramSolver {
         t = clip0_hi_fast(x1 - g1 * r1, hi_of(x0));
         s = t - x1; x1 = t;
         g0 += s * G01; g1 += s * G11; g3 += s * G13; g4 += s * G14;
-        t = -(g1 - g0) * r3a;
-        t = BOX ? clip_sym(t, x1, x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
-        x0 = x0 - t; x1 = x1 + t;
-        g0 += t * SA0; g1 += t * SA1; g3 += t * SA3; g4 += t * SA4;
+        if (TC_SLIDE_ONE && BOX && !IsStrict<R>::value) {
+            slide_one(x0, x1, (g1 - g0) * r3a, s);
+            g0 -= s * SA0; g1 -= s * SA1; g3 -= s * SA3; g4 -= s * SA4;
+        } else {
+            t = -(g1 - g0) * r3a;
+            t = BOX ? clip_sym(t, x1, x0) : clipv(t, -maxv(x1, R(0)), maxv(x0, R(0)));
+            x0 = x0 - t; x1 = x1 + t;
+            g0 += t * SA0; g1 += t * SA1; g3 += t * SA3; g4 += t * SA4;
+        }
         t = clip0_hi_fast(x2 - g3 * r2, hi_of(x3));
         s = t - x2; x2 = t;
         g0 += s * G03; g1 += s * G13; g3 += s * G33; g4 += s * G34;
         t = clip0_hi_fast(x3 - g4 * r3, hi_of(x2));
         s = t - x3; x3 = t;
         g0 += s * G04; g1 += s * G14; g3 += s * G34; g4 += s * G44;
-        t = -(g4 - g3) * r3b;
-        t = BOX ? clip_sym(t, x3, x2) : clipv(t, -maxv(x3, R(0)), maxv(x2, R(0)));
-        x2 = x2 - t; x3 = x3 + t;
-        g0 += t * SB0; g1 += t * SB1; g3 += t * SB3; g4 += t * SB4;
+        if (TC_SLIDE_ONE && BOX && !IsStrict<R>::value) {
+            slide_one(x2, x3, (g4 - g3) * r3b, s);
+            g0 -= s * SB0; g1 -= s * SB1; g3 -= s * SB3; g4 -= s * SB4;
+        } else {
+            t = -(g4 - g3) * r3b;
+            t = BOX ? clip_sym(t, x3, x2) : clipv(t, -maxv(x3, R(0)), maxv(x2, R(0)));
+            x2 = x2 - t; x3 = x3 + t;
+            g0 += t * SB0; g1 += t * SB1; g3 += t * SB3; g4 += t * SB4;
+        }
     }
 
     // Epilogue.  The pair is re-read (shared-memory copy) where needed, so
