@@ -365,7 +365,7 @@ def main():
         "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write)",
         "traffic_source": traffic_note, "algorithmic_bytes_per_launch": n * bytes_per_pair,
         "kernel": ("hybrid_kernel<double,strict,soa>" if args.strict else
-                   "hybrid_ws_kernel<double,fast,soa,12,1> (warp-specialised: 12 iterative + 4 fallback warps per SM)"),
+                   "hybrid_ws_kernel<double,fast,soa,12,1,full> (warp-specialised: 12 iterative + 4 fallback warps per SM)"),
         "kernel_ms": ms_kernel,
         "flops_per_launch": flops,
         "flop_model": "SURVEY.md 8(d)/App. A algorithmic work: n(200+88N) + 1199 fallback + 254 fallback&intersect "
@@ -786,7 +786,7 @@ def roofline_f32(D, torch, lib, ta, tb, n, dev, stream, reps=5):
     flops = flops_reference_model(n, PARAMS["n_iterative"], s["fallback"], s["intersecting"])
     peak = fma_peak(torch, lib, stream, dev, fp64=False)
     achieved = flops / (ms / 1e3) / 1e12
-    return {"bound": "fp32", "kernel": "hybrid_ws_kernel<float,fast,soa,16,2> (warp-specialised: 16 iterative + 8 fallback warps per SM)", "achieved": achieved, "peak": peak,
+    return {"bound": "fp32", "kernel": "hybrid_ws_kernel<float,fast,soa,16,2,full> (warp-specialised: 16 iterative + 8 fallback warps per SM)", "achieved": achieved, "peak": peak,
             "unit": "TFLOP/s", "frac": achieved / peak, "kernel_ms": ms, "pairs_per_s": n / (ms / 1e3),
             "fallback_rate": s["fallback"] / n, "flops_per_launch": flops,
             "flop_model": "SURVEY.md 8(d)/App. A, as roofline", "peak_source": "in-run FFMA probe (tc_fma_probe)",

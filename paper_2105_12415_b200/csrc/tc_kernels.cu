@@ -878,15 +878,22 @@ constexpr int WS_FB = 128;           // threads of one fallback warpgroup (= one
 constexpr int WS_Q2 = TC_WS_Q2;      // phase-2 stack entries per warpgroup (< 2 WS_FB: phase-1 batches shrink to fit)
 constexpr int WS_NBUF = TC_WS_ASYNC ? 2 : 1;  // stash buffers per iterative warp
 static_assert(WS_Q2 >= WS_FB + 32 && WS_Q2 <= 2 * WS_FB, "phase-2 stack size");
-constexpr int64_t WS_FREE = -1;
 
+constexpr int64_t WS_FREE = -1;
 struct WsGroup {
     int64_t q2[WS_Q2];  // pair index (| IDS_ONLY) of each phase-2 stack entry
     int n2, m, pos;
 };
 template <int FWG>
 struct WsShared {
-    int64_t ring[WS_RING];  // pair index of each ring slot; WS_FREE = free
+    int64_t ring[WS_RING];  // pair index of each ring slot (one consumer group: WS_FREE = free)
+    // Slot sequence numbers (bounded multi-producer / multi-consumer queue; used with FWG > 1):
+    // slot q starts at q; the producer holding position p waits for seq == p,
+    // fills the slot and sets p + 1; the consumer holding p waits for p + 1,
+    // reads and sets p + WS_RING (free for the next lap).  With two fallback
+    // warpgroups a claim a whole lap ahead of the other group's unfinished
+    // batch can therefore never take the previous lap's entry for its own.
+    int seq[WS_RING];
     WsGroup g[FWG];
     int tail, head, done;
 };
@@ -936,7 +943,11 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
     extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
     T* const ringd = reinterpret_cast<T*>(tc_dyn_smem);
     Tally tl;
-    for (int k = threadIdx.x; k < WS_RING; k += WS_BS) S.ring[k] = WS_FREE;
+    constexpr bool SEQ = WS_FWG > 1;  // several consumers: sequence-numbered slots (WsShared)
+    for (int k = threadIdx.x; k < WS_RING; k += WS_BS) {
+        S.seq[k] = k;
+        S.ring[k] = WS_FREE;
+    }
     if (threadIdx.x == 0) {
         S.tail = S.head = S.done = 0;
         for (int g = 0; g < WS_FWG; ++g) S.g[g].n2 = S.g[g].m = S.g[g].pos = 0;
@@ -1022,9 +1033,13 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
                 if (lane == 0) base = atomicAdd(&S.tail, __popc(m));
                 base = __shfl_sync(0xffffffffu, base, 0);
                 if (enq) {
-                    const int q = (unsigned)(base + __popc(m & ((1u << lane) - 1u))) % (unsigned)WS_RING;
+                    const int pos = base + __popc(m & ((1u << lane) - 1u));
+                    const int q = (unsigned)pos % (unsigned)WS_RING;
+                    volatile int* sq = &S.seq[q];
                     volatile int64_t* idx = &S.ring[q];
-                    while (*idx != WS_FREE) __nanosleep(64);  // ring full: the fallback frees slots
+                    // ring full: the fallback frees slots
+                    if (SEQ) while (*sq != pos) __nanosleep(64);
+                    else while (*idx != WS_FREE) __nanosleep(64);
                     ws_fence();  // the slot's previous reader is done before we overwrite it
                     if (PAIRED) {
 #pragma unroll
@@ -1037,9 +1052,11 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
 #pragma unroll
                         for (int k = 0; k < 18; ++k) ringd[k * WS_RING + q] = slot[k * 32];
                     }
-                    // the coordinates and the placeholder row before the index
+                    if (SEQ) *idx = i;
+                    // the slot and the placeholder row before the sequence number / index
                     ws_fence();
-                    *idx = i;
+                    if (SEQ) *sq = pos + 1;
+                    else *idx = i;
                 }
             }
         }
@@ -1119,9 +1136,13 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
             const int q = (unsigned)(pos + ft) % (unsigned)WS_RING;
             int64_t j = -1;
             if (ft < m) {
+                volatile int* sq = &S.seq[q];
                 volatile int64_t* idx = &S.ring[q];
-                while ((j = *idx) == WS_FREE) __nanosleep(32);  // claimed by a producer, not yet written
+                // claimed by a producer, not yet written
+                if (SEQ) while (*sq != pos + ft + 1) __nanosleep(32);
+                else while ((j = *idx) == WS_FREE) __nanosleep(32);
                 ws_fence();
+                if (SEQ) j = *idx;
             }
             bool push2 = false;
             int64_t e2 = 0;
@@ -1166,7 +1187,10 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
             }
             // every read of the ring slot (phase 1, the copy) before it is freed
             ws_fence();
-            if (ft < m) *(volatile int64_t*)&S.ring[q] = WS_FREE;
+            if (ft < m) {  // free for the next lap
+                if (SEQ) *(volatile int*)&S.seq[q] = pos + ft + WS_RING;
+                else *(volatile int64_t*)&S.ring[q] = WS_FREE;
+            }
             fb_sync(gi);  // q2 entries visible, G.m / G.pos read by everyone
             phase2_batches(false);
         }

@@ -13,6 +13,11 @@ namespace tc {
 // loops: full unrolling makes every vertex index a compile-time constant.
 // Measured: X fully unrolled (3) is 3.5 % faster for the comparison kernel
 // and 1.2 % for the hybrid; unrolling F (3 or 9) is 4-7 % slower (spills).
+// experiment: let the three unrolled segment tests interleave (needs > 128
+// registers: measured with setmaxnreg roles, 120 / 152: hybrid +2.7 %)
+#ifndef TC_P2_INTERLEAVE
+#define TC_P2_INTERLEAVE 0
+#endif
 #ifndef TC_UNROLL_X
 #define TC_UNROLL_X 3
 #endif
@@ -621,7 +626,7 @@ __device__ __forceinline__ void comparison_phase2_impl(const Tri& A, const Tri& 
         for (int kb = 0; kb < 3; ++kb) {
             // (keeps the unrolled tests from being interleaved: the next
             // test's loads stay behind this point, so one test is live at a time)
-            asm volatile("" ::: "memory");
+            if (!TC_P2_INTERLEAVE) asm volatile("" ::: "memory");
             R p2[3], q2[3], s, t, d2;
             B.vertex(edge_start(kb), p2);
             B.vertex(edge_end(kb), q2);
