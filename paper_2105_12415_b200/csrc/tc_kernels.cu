@@ -874,8 +874,11 @@ __global__ void __launch_bounds__(BS_HYB, sizeof(T) == 4 ? TC_HYB_CTAS_F32 : TC_
 #define TC_WS_Q2 256
 #endif
 constexpr int WS_RING = TC_WS_RING;  // ring slots (256: 2.347 ms -- producers wait; 512-768: 2.08)
-constexpr int WS_FB = 128;           // threads of one fallback warpgroup (= one batch)
-constexpr int WS_Q2 = TC_WS_Q2;      // phase-2 stack entries per warpgroup (< 2 WS_FB: phase-1 batches shrink to fit)
+#ifndef TC_WS_FB
+#define TC_WS_FB 128
+#endif
+constexpr int WS_FB = TC_WS_FB;      // threads of one fallback warpgroup (= one batch)
+constexpr int WS_Q2 = TC_WS_Q2 < 2 * WS_FB ? TC_WS_Q2 : 2 * WS_FB;      // phase-2 stack entries per warpgroup (< 2 WS_FB: phase-1 batches shrink to fit)
 constexpr int WS_NBUF = TC_WS_ASYNC ? 2 : 1;  // stash buffers per iterative warp
 static_assert(WS_Q2 >= WS_FB + 32 && WS_Q2 <= 2 * WS_FB, "phase-2 stack size");
 
@@ -937,6 +940,7 @@ template <typename T, bool STRICT, bool SOA, int WS_IW, int WS_FWG, bool FULL>
 __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kernel(Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     constexpr bool PAIRED = sizeof(T) == 8 ? TC_WS_PAIRED_F64 : TC_WS_PAIRED_F32;
+    static_assert(!(TC_WS_ASYNC && PAIRED), "the cp.async tiles land in planar layout");
     constexpr int WS_IT = 32 * WS_IW;  // iterative threads
     constexpr int WS_BS = WS_IT + WS_FWG * WS_FB;
     __shared__ WsShared<WS_FWG> S;

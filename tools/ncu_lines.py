@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
 
-    python tools/ncu_lines.py gpurun_out/prof.ncu-rep <kernel-substring> [lib.so] [top]
+    python tools/ncu_lines.py gpurun_out/prof.ncu-rep <kernel-substring> [lib.so] [top] [mangled-substring]
 
 Reads the SASS source page of the report (per-instruction stall samples) and
 the line table of the cubin inside the library (nvdisasm -g), then prints the
@@ -73,6 +73,8 @@ def main():
     kname = next(k for k in samples if ksub in k)
     mangled = {"hybrid": "hybrid_kernelIdLb0ELb1", "iterative": "iterative_kernelIdLb0ELb1",
                "comparison": "comparison_kernelIdLb0ELb1"}.get(ksub, ksub)
+    if len(sys.argv) > 5:  # mangled-name substring given separately from the demangled one
+        mangled = sys.argv[5]
     table = line_table(lib, mangled)
     by_line = collections.Counter()
     total = 0

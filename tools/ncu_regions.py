@@ -36,7 +36,7 @@ REGIONS = [
     ("phase2", "tc_pair.cuh", r"void comparison_phase2_impl\("),
     ("degenerate", "tc_pair.cuh", r"bool degenerate_tri_t\("),
     ("stage_pair", "tc_kernels.cu", r"void stage_pair\("),
-    ("store_rec", "tc_kernels.cu", r"void store_rec\("),
+    ("store_rec", "tc_kernels.cu", r"void store_rec(_full)?\("),
     ("load_tri", "tc_kernels.cu", r"void load_tri\("),
     ("stash_pair", "tc_kernels.cu", r"void stash_pair\("),
     ("push", "tc_kernels.cu", r"void push\(int64_t\* q"),
@@ -119,11 +119,14 @@ def main():
     lib = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "paper_2105_12415_b200", "libtricontact_b200.so")
     sp = spans()
     chains = line_chains(lib, mangled)
-    m = re.match(r"(\w+?)I([df])Lb([01])ELb([01])E?(?:Li(\d+)ELi(\d+)E)?", mangled)
+    m = re.match(r"(\w+?)I([df])Lb([01])ELb([01])E?(?:Li(\d+)ELi(\d+)E)?(?:Lb([01])E)?", mangled)
     ksub = mangled
     if m:
         ksub = f"{m.group(1)}<{'double' if m.group(2) == 'd' else 'float'}, (bool){m.group(3)}, (bool){m.group(4)}"
-        ksub += f", (int){m.group(5)}, (int){m.group(6)}>" if m.group(5) else ">"
+        if m.group(5):
+            ksub += f", (int){m.group(5)}, (int){m.group(6)}" + (f", (bool){m.group(7)}>" if m.group(7) else ">")
+        else:
+            ksub += ">"
     rows = sass_rows(rep, ksub)
     base = min(a for a, *_ in rows)
     agg = collections.defaultdict(lambda: collections.Counter())
