@@ -125,6 +125,11 @@ struct Args {
     tc_stats* stats;
     double c_factor, alpha_it, alpha_reg, move_factor, start_coord;
     int n_iterative;
+    // library-owned cumulative counters {pairs, fallbacks} of the warp-specialised hybrid's
+    // launches on this device (fallback_history): device memory, and the host-mapped
+    // copy CTA 0 refreshes; or NULL
+    unsigned long long* hist = nullptr;
+    unsigned long long* hist_host = nullptr;
 };
 
 template <class R, class A>
@@ -370,8 +375,8 @@ struct Tally {
 
     // COMPARISON_IS_FALLBACK: hybrid comparisons also count as fallbacks
     template <bool COMPARISON_IS_FALLBACK, int NWARPS = BLOCK / 32>
-    __device__ void flush(tc_stats* s) {
-        if (!s) return;
+    __device__ void flush(tc_stats* s, unsigned long long* hist = nullptr, unsigned long long* hist_host = nullptr) {
+        if (!s && !hist) return;
         __shared__ unsigned long long red[5][NWARPS];  // iterative, comparison, degenerate, contacts, intersecting
         __shared__ double redm[NWARPS];
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -400,6 +405,19 @@ struct Tally {
                 for (int k = 0; k < 5; ++k) v[k] += red[k][w];
                 m = (redm[w] < m) ? redm[w] : m;
             }
+            if (hist) {
+                atomicAdd(hist, v[0]);
+                atomicAdd(hist + 1, v[1] + v[2]);
+                if (blockIdx.x == 0) {
+                    // two posted writes to host memory per launch (per-CTA system-scope
+                    // reductions over PCIe cost 0.2 ms per launch); the totals of CTAs
+                    // still running reach the host with the next launch
+                    __threadfence();
+                    ((volatile unsigned long long*)hist_host)[0] = ((volatile unsigned long long*)hist)[0];
+                    ((volatile unsigned long long*)hist_host)[1] = ((volatile unsigned long long*)hist)[1];
+                }
+            }
+            if (!s) return;
             auto* c = reinterpret_cast<unsigned long long*>(s);
             if (v[0]) atomicAdd(c + 0, v[0]);
             if (v[1]) {
@@ -900,12 +918,27 @@ struct WsShared {
     WsGroup g[FWG];
     int tail, head, done;
 };
+// TC_WS_SELF: when the ring is nearly full (the fallback warps are behind: a
+// batch with many open pairs, e.g. BASELINE config 3's near-parallel class at
+// 84 % fallbacks), an iterative warp runs the comparison phases for its own
+// tile's open pairs, straight from its stash, instead of sleeping on a full
+// ring -- the static 12 + 4 split of the warps then degrades towards the fused
+// kernel's behaviour instead of towards four warps' throughput.
+// TC_WS_SELF_MARGIN: serve locally when fewer than this many ring positions are unclaimed.
+// TC_WS_SELF: 0 never, 1 chosen per launch from the device's fallback history, 2 always.
+#ifndef TC_WS_SELF
+#define TC_WS_SELF 1
+#endif
+#ifndef TC_WS_SELF_MARGIN
+#define TC_WS_SELF_MARGIN 192
+#endif
 // dynamic shared memory (T elements): [ring coordinates 18 x WS_RING]
 // [per warpgroup: phase-2 coordinates 18 x WS_Q2, crossing scratch SCR x WS_FB]
 // [iterative stash 18 x 32 IW]
 template <typename T, int IW, int FWG>
-constexpr size_t ws_smem_bytes() {
-    return sizeof(T) * (18 * WS_RING + FWG * (18 * WS_Q2 + SCR * WS_FB) + WS_NBUF * 18 * 32 * IW);
+constexpr size_t ws_smem_bytes(bool self) {
+    return sizeof(T) * (18 * WS_RING + FWG * (18 * WS_Q2 + SCR * WS_FB) + WS_NBUF * 18 * 32 * IW +
+                        (self ? SCR * 32 * IW : 0));
 }
 // Producer / consumer ordering inside the CTA.  TC_WS_FENCE 1: fence.acq_rel.cta
 // instead of __threadfence_block() (fence.sc.cta, MEMBAR.SC): release /
@@ -936,8 +969,59 @@ __device__ __forceinline__ void ws_fence() {
 // named barrier of fallback warpgroup g (ids 1..FWG; 0 is __syncthreads)
 __device__ __forceinline__ void fb_sync(int g) { asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(WS_FB) : "memory"); }
 
-template <typename T, bool STRICT, bool SOA, int WS_IW, int WS_FWG, bool FULL>
-__global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kernel(Args<T> a) {
+// TC_WS_SELF cold path: the degenerate screen and both comparison phases for
+// one open pair read from an iterative warp's stash (planar [18][32] or paired
+// words), results stored like the fallback warpgroup's; returns the tally
+// contributions (1 degenerate, 2 compared, 4 contact, 8 intersecting) and the distance.
+struct ServeOut {
+    unsigned flags;
+    double dist;
+};
+template <typename T, bool STRICT, bool SOA, bool FULL, bool PAIRED>
+__device__ __noinline__ ServeOut ws_self_serve(const Args<T>* ap, int64_t i, const T* stash, T* scr_p) {
+    using R = typename Pol<T, STRICT>::R;
+    const Args<T>& a = *ap;
+    Scratch<R> scr;
+    scr.p = scr_p;
+    scr.stride = 32;
+    const FlatSource<SOA, R, T, 32, FULL> src{a, nullptr};  // (stores only)
+    const R eps = R(a.eps ? a.eps[i] : a.eps_scalar);
+    ServeOut out{0u, 0.0};
+    auto serve = [&](const auto& TA, const auto& TB) {
+        Rec<R> r;
+        if (degenerate_tri_t<R>(TA) || degenerate_tri_t<R>(TB)) {
+            src.mark_degenerate(i);
+            out.flags = 1u;
+            return;
+        }
+        if (comparison_phase1(TA, TB, eps, scr, r)) {
+            r.ids |= (uint32_t)FLAG_FALLBACK << 24;
+            src.store(i, r);
+            if (!FULL && a.ids != nullptr) {
+                Rec<R> r2;
+                comparison_phase2(TA, TB, eps, true, r2, scr);
+                src.store_ids01(i, r2.ids);
+            }
+        } else {
+            comparison_phase2(TA, TB, eps, false, r, scr);
+            r.ids |= (uint32_t)FLAG_FALLBACK << 24;
+            src.store(i, r);
+        }
+        out.flags = 2u | (r.kind == KIND_CONTACT ? 4u : 0u) | (((r.ids >> 24) & FLAG_INTERSECT) ? 8u : 0u);
+        out.dist = (double)val(r.distance);
+    };
+    if constexpr (PAIRED) {
+        using T2 = typename Vec2<T>::type;
+        const T2* s2 = reinterpret_cast<const T2*>(stash);
+        serve(PairTri<R>{s2, 0}, PairTri<R>{s2, 9});
+    } else {
+        serve(SmemTri<R>{stash, 32}, SmemTri<R>{stash + 9 * 32, 32});
+    }
+    return out;
+}
+
+template <typename T, bool STRICT, bool SOA, int WS_IW, int WS_FWG, bool FULL, bool SELF>
+__global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kernel(const __grid_constant__ Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     constexpr bool PAIRED = sizeof(T) == 8 ? TC_WS_PAIRED_F64 : TC_WS_PAIRED_F32;
     static_assert(!(TC_WS_ASYNC && PAIRED), "the cp.async tiles land in planar layout");
@@ -1032,7 +1116,35 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
                 if (!enq) tl.result(r);
             }
             const unsigned m = __ballot_sync(0xffffffffu, enq);
-            if (m) {
+            bool self = false;
+            if (SELF && m) {
+                int occ = 0;
+                if (lane == 0) occ = *(volatile int*)&S.tail - *(volatile int*)&S.head;
+                self = __shfl_sync(0xffffffffu, occ, 0) > WS_RING - TC_WS_SELF_MARGIN;
+            }
+            if (self) {
+                if (enq) {
+                    // the comparison phases for this lane's open pair, read from the warp's stash
+                    // (a separate function: the cold path stays out of the sweep's register allocation)
+                    T* const scr_p = ringd + 18 * WS_RING + WS_FWG * (18 * WS_Q2 + SCR * WS_FB) +
+                                     WS_NBUF * 18 * 32 * WS_IW + wid * (SCR * 32) + lane;  // (allocated with SELF)
+#ifndef TC_X_SELF_NOCALL  // timing-only
+#define TC_X_SELF_NOCALL 0
+#endif
+                    const ServeOut so = TC_X_SELF_NOCALL ? ServeOut{0u, (double)(scr_p - slot)} :
+                        ws_self_serve<T, STRICT, SOA, FULL, PAIRED>(
+                        &a, i, PAIRED ? reinterpret_cast<const T*>(slot2) : slot, scr_p);
+                    tl.degenerate += so.flags & 1u;
+                    if (so.flags & 2u) {
+                        tl.comparison++;
+                        tl.contacts += (so.flags >> 2) & 1u;
+                        tl.intersecting += (so.flags >> 3) & 1u;
+                        const double d = so.dist + 0.0;
+                        tl.min_d = (d < tl.min_d) ? d : tl.min_d;
+                    }
+                }
+                __syncwarp();
+            } else if (m) {
                 int base = 0;
                 if (lane == 0) base = atomicAdd(&S.tail, __popc(m));
                 base = __shfl_sync(0xffffffffu, base, 0);
@@ -1200,7 +1312,14 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
         }
         phase2_batches(true);
     }
-    tl.flush<true, WS_BS / 32>(a.stats);
+    if (TC_DEBUG) {  // every pushed pair was claimed, both phase-2 stacks are empty
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            TC_CHECK(S.head == S.tail && S.done == WS_IW);
+            for (int g = 0; g < WS_FWG; ++g) TC_CHECK(S.g[g].n2 == 0);
+        }
+    }
+    tl.flush<true, WS_BS / 32>(a.stats, a.hist, a.hist_host);
 }
 
 // ---- warp-specialised hybrid, warp-granular fallback (TC_WSW) ---------------------------
@@ -1940,6 +2059,57 @@ static int sm_count() {
     return v;
 }
 
+// Per-device history of the warp-specialised hybrid's fallback rate.  Every CTA of
+// that kernel adds its pair and fallback counts to two cumulative device counters
+// and CTA 0 copies them to host-mapped memory (two posted writes at the end of
+// the kernel: no stream operation, no synchronisation); a launch reads
+// whatever has landed and, once at least 2^16
+// more pairs are accounted for, refreshes the rate.  A rate above TC_WS_SELF_RATE
+// selects the kernel instance whose iterative warps serve their own open
+// pairs when the ring is nearly full (TC_WS_SELF) -- the first launches of a
+// process, and launches after a change of workload, run the plain instance.
+#ifndef TC_WS_SELF_RATE
+#define TC_WS_SELF_RATE 0.6
+#endif
+struct FallbackHistory {
+    unsigned long long* counters = nullptr;      // host-mapped {pairs, fallbacks}
+    unsigned long long* dev_counters = nullptr;  // the kernels' cumulative counters (device memory)
+    std::atomic<unsigned long long> seen_pairs{0}, seen_fb{0};
+    std::atomic<int> is_high{0};
+    std::once_flag once;
+    bool high() {
+        if (!dev_counters) return false;
+        const unsigned long long p = ((volatile unsigned long long*)counters)[0];
+        const unsigned long long f = ((volatile unsigned long long*)counters)[1];
+        const unsigned long long p0 = seen_pairs.load(std::memory_order_relaxed);
+        const unsigned long long f0 = seen_fb.load(std::memory_order_relaxed);
+        if (p >= p0 + 65536 && f >= f0) {
+            is_high.store((double)(f - f0) > TC_WS_SELF_RATE * (double)(p - p0), std::memory_order_relaxed);
+            seen_pairs.store(p, std::memory_order_relaxed);
+            seen_fb.store(f, std::memory_order_relaxed);
+        }
+        return is_high.load(std::memory_order_relaxed) != 0;
+    }
+};
+static FallbackHistory& fallback_history() {
+    static FallbackHistory hist[kMaxDevices];
+    FallbackHistory& h = hist[current_device()];
+    std::call_once(h.once, [&h] {
+        void *p = nullptr, *d = nullptr;
+        if (cudaHostAlloc(&p, 2 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) ==
+                cudaSuccess &&
+            cudaMalloc(&d, 2 * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMemset(d, 0, 2 * sizeof(unsigned long long)) == cudaSuccess) {
+            memset(p, 0, 2 * sizeof(unsigned long long));
+            h.counters = static_cast<unsigned long long*>(p);
+            h.dev_counters = static_cast<unsigned long long*>(d);
+        } else {
+            cudaGetLastError();  // no history: the plain instance every time
+        }
+    });
+    return h;
+}
+
 template <typename K>
 static int64_t grid_for(K kernel, int64_t n, size_t smem = 0, int threads = BLOCK) {
     if (smem > 16 * 1024) {
@@ -2002,8 +2172,18 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         constexpr int FWG = sizeof(T) == 8 ? TC_WS_FWG_F64 : TC_WS_FWG_F32;
         // the full-record instance (every column, no ids) has no per-column null tests
         const bool full = TC_WS_FULL && full_record(a);
-        auto k = full ? hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, true> : hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, false>;
-        const size_t smem = ws_smem_bytes<T, IW, FWG>();
+        // the self-serving instance when this device's recent launches fell back a lot (fallback_history)
+        FallbackHistory& fh = fallback_history();
+        const bool self = TC_WS_SELF == 2 || (TC_WS_SELF == 1 && fh.high());
+        Args<T> aw = a;
+        aw.hist = TC_WS_SELF == 1 ? fh.dev_counters : nullptr;
+        aw.hist_host = fh.counters;
+        const Args<T>& a = aw;
+        auto k = full ? (self ? hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, true, true>
+                              : hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, true, false>)
+                      : (self ? hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, false, true>
+                              : hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, false, false>);
+        const size_t smem = ws_smem_bytes<T, IW, FWG>(self);
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int64_t ctas = (a.n + 32 * IW - 1) / (32 * IW);
         int64_t g = ctas < sm_count() ? ctas : sm_count();
@@ -2812,6 +2992,7 @@ int tc_allreduce_stats(tc_stats* stats, void* nccl_comm, void* stream) {
 }
 
 void tc_debug_set_max_ctas(int64_t max_ctas) { tc::g_max_ctas.store(max_ctas > 0 ? max_ctas : 0); }
+int tc_debug_fallback_rate_high(void) { return TC_WS_SELF == 1 && tc::fallback_history().high() ? 1 : 0; }
 
 void* tc_host_alloc(int64_t bytes) { return tc::host_alloc(bytes); }
 int tc_host_free(void* p) { return tc::host_free(p); }

@@ -57,3 +57,54 @@ def test_release_determinism_and_cap_invariance(strict):
                 assert np.array_equal(ref[k], cur[k]), (cap, k)
     finally:
         lib.tc_debug_set_max_ctas(0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_self_serving_instance_equals_plain(dtype):
+    """The fast hybrid's self-serving instance (iterative warps run the comparison
+    phases for their own open pairs when the ring is nearly full) is selected from
+    the device's fallback history: a batch with ~84 % fallbacks (cfg3 near-parallel
+    faces) switches it on, ordinary cfg1 pairs switch it off again, and every
+    column, the ids and the counters equal the plain instance's bit for bit -- with
+    and without feature ids, per-pair halos and an allow mask."""
+    lib = _abi.load()
+    n = 1 << 17
+    A3, B3 = W.adversarial_pairs(n)
+    hot = torch.from_numpy(W.to_soa(A3[:n], B3[:n])).cuda().to(dtype)  # class 0: near-parallel
+    A1, B1 = W.random_pairs(n, seed=43, sep=(0.3, 0.5))  # well separated: few fallbacks
+    cold = torch.from_numpy(W.to_soa(A1, B1)).cuda().to(dtype)
+    P = D.Params(n_iterative=16, epsilon=1e-6)
+    rng = np.random.default_rng(5)
+    eps = torch.from_numpy(rng.uniform(5e-7, 2e-6, n)).cuda().to(dtype)
+    allow = torch.from_numpy((rng.random(n) < 0.9).astype(np.uint8)).cuda()
+
+    def run(pl, **kw):
+        st = D.new_stats()
+        out = D.run("hybrid", pl[:9], pl[9:], P, soa=True, stats=st, **kw)
+        torch.cuda.synchronize()
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        res["stats"] = np.array(list(D.read_stats(st).values()))
+        return res
+
+    def settle(pl, want):
+        # the history needs 2^16 freshly counted pairs: a few synchronised launches
+        for _ in range(6):
+            run(pl)
+            if lib.tc_debug_fallback_rate_high() == want:
+                return
+        raise AssertionError(f"fallback history did not reach {want}")
+
+    settle(cold, 0)
+    plain = [run(hot), ]                       # launched with the plain instance
+    settle(hot, 1)
+    served = [run(hot), run(hot, ids=True), run(hot, ids=True, eps=eps, allow=allow)]
+    assert lib.tc_debug_fallback_rate_high() == 1
+    settle(cold, 0)
+    plain += [run(hot, ids=True), ]            # plain again (the launch reads the history first)
+    settle(cold, 0)
+    plain += [run(hot, ids=True, eps=eps, allow=allow)]
+    assert served[0]["stats"][2] > 0.7 * n     # the batch does fall back
+    for a, b in zip(plain, served):
+        assert a.keys() == b.keys()
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k

@@ -22,12 +22,18 @@ ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--strict", action="store_true")
 ap.add_argument("--variant", default="hybrid")
 ap.add_argument("--no-fallback", action="store_true", help="hybrid with an all-zero allow mask")
+ap.add_argument("--cfg3", type=int, default=-1, help="time class k (0-3) of the adversarial set, 2^20 pairs, instead of cfg1")
 args = ap.parse_args()
 dt = torch.float64 if args.dtype == "f64" else torch.float32
 n = args.n
 planes = torch.empty((18, n), dtype=torch.float64, device="cuda")
 lib0 = _abi.load()
 _abi.check(lib0.tc_random_pairs_soa_f64(0, 0, n, -0.1, 0.5, ctypes.c_void_p(planes.data_ptr()), None), "gen")
+if args.cfg3 >= 0:
+    n = 1 << 20
+    A3, B3 = W.adversarial_pairs(n)
+    sl = slice(args.cfg3 * n, (args.cfg3 + 1) * n)
+    planes = torch.from_numpy(W.to_soa(A3[sl], B3[sl])).to("cuda")
 planes = planes.to(dt)
 ta, tb = planes[:9], planes[9:]
 out = D.alloc_outputs(n, dt, "cuda", soa=True)
