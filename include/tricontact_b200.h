@@ -275,12 +275,16 @@ int tc_random_pairs_soa_f64(uint64_t seed, int64_t start, int64_t n, double sep_
  * fallback queues and batches, so result equality across caps exposes
  * ordering / synchronisation faults (tests/test_gpu_stress.py). */
 void tc_debug_set_max_ctas(int64_t max_ctas);
-/* The fast hybrid keeps, per device, the fallback rate of its recent launches
- * (cumulative pair / fallback counters the kernels update; no synchronisation)
- * and launches the instance whose iterative warps also serve their own open
- * pairs when that rate is high.  Returns 1 if the calling thread's current
- * device would get that instance now, 0 if not (tests/test_gpu_stress.py). */
+/* The fast hybrid keeps, per device, a history of its recent launches
+ * (cumulative counters the kernels update; no synchronisation): when the
+ * iterative warps found the hand-over ring full, the next launches use the
+ * instance whose iterative warps also serve their own open pairs.  Returns 1
+ * if the calling thread's current device would get that instance now, 0 if
+ * not (tests/test_gpu_stress.py). */
 int tc_debug_fallback_rate_high(void);
+/* The history's cumulative counters as last published by a kernel: pairs,
+ * fallbacks, ring waits of the iterative warps (per lane and poll), self-served tiles. */
+void tc_debug_fallback_history(uint64_t out[4]);
 /* Number of kernel launches this library has enqueued since load. */
 int64_t tc_launch_count(void);
 

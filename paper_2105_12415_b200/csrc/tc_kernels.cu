@@ -375,7 +375,8 @@ struct Tally {
 
     // COMPARISON_IS_FALLBACK: hybrid comparisons also count as fallbacks
     template <bool COMPARISON_IS_FALLBACK, int NWARPS = BLOCK / 32>
-    __device__ void flush(tc_stats* s, unsigned long long* hist = nullptr, unsigned long long* hist_host = nullptr) {
+    __device__ void flush(tc_stats* s, unsigned long long* hist = nullptr, unsigned long long* hist_host = nullptr,
+                          unsigned ring_waits = 0, unsigned self_tiles = 0) {  // (the CTA's, read by thread 0)
         if (!s && !hist) return;
         __shared__ unsigned long long red[5][NWARPS];  // iterative, comparison, degenerate, contacts, intersecting
         __shared__ double redm[NWARPS];
@@ -408,13 +409,15 @@ struct Tally {
             if (hist) {
                 atomicAdd(hist, v[0]);
                 atomicAdd(hist + 1, v[1] + v[2]);
+                if (ring_waits) atomicAdd(hist + 2, (unsigned long long)ring_waits);
+                if (self_tiles) atomicAdd(hist + 3, (unsigned long long)self_tiles);
                 if (blockIdx.x == 0) {
                     // two posted writes to host memory per launch (per-CTA system-scope
                     // reductions over PCIe cost 0.2 ms per launch); the totals of CTAs
                     // still running reach the host with the next launch
                     __threadfence();
-                    ((volatile unsigned long long*)hist_host)[0] = ((volatile unsigned long long*)hist)[0];
-                    ((volatile unsigned long long*)hist_host)[1] = ((volatile unsigned long long*)hist)[1];
+                    for (int k = 0; k < 4; ++k)
+                        ((volatile unsigned long long*)hist_host)[k] = ((volatile unsigned long long*)hist)[k];
                 }
             }
             if (!s) return;
@@ -917,6 +920,7 @@ struct WsShared {
     int seq[WS_RING];
     WsGroup g[FWG];
     int tail, head, done;
+    unsigned ring_waits, self_tiles;  // polls of producers on a full ring; tiles served by their own warp
 };
 // TC_WS_SELF: when the ring is nearly full (the fallback warps are behind: a
 // batch with many open pairs, e.g. BASELINE config 3's near-parallel class at
@@ -1038,6 +1042,7 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
     }
     if (threadIdx.x == 0) {
         S.tail = S.head = S.done = 0;
+        S.ring_waits = S.self_tiles = 0;
         for (int g = 0; g < WS_FWG; ++g) S.g[g].n2 = S.g[g].m = S.g[g].pos = 0;
     }
     __syncthreads();
@@ -1123,6 +1128,7 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
                 self = __shfl_sync(0xffffffffu, occ, 0) > WS_RING - TC_WS_SELF_MARGIN;
             }
             if (self) {
+                if (lane == 0) atomicAdd(&S.self_tiles, 1u);
                 if (enq) {
                     // the comparison phases for this lane's open pair, read from the warp's stash
                     // (a separate function: the cold path stays out of the sweep's register allocation)
@@ -1154,8 +1160,10 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
                     volatile int* sq = &S.seq[q];
                     volatile int64_t* idx = &S.ring[q];
                     // ring full: the fallback frees slots
-                    if (SEQ) while (*sq != pos) __nanosleep(64);
-                    else while (*idx != WS_FREE) __nanosleep(64);
+                    unsigned polls = 0;
+                    if (SEQ) while (*sq != pos) { __nanosleep(64); ++polls; }
+                    else while (*idx != WS_FREE) { __nanosleep(64); ++polls; }
+                    if (polls) atomicAdd(&S.ring_waits, polls);  // (rare: the fallback-history signal)
                     ws_fence();  // the slot's previous reader is done before we overwrite it
                     if (PAIRED) {
 #pragma unroll
@@ -1319,7 +1327,8 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
             for (int g = 0; g < WS_FWG; ++g) TC_CHECK(S.g[g].n2 == 0);
         }
     }
-    tl.flush<true, WS_BS / 32>(a.stats, a.hist, a.hist_host);
+    __syncthreads();  // the history counters are final
+    tl.flush<true, WS_BS / 32>(a.stats, a.hist, a.hist_host, S.ring_waits, S.self_tiles);
 }
 
 // ---- warp-specialised hybrid, warp-granular fallback (TC_WSW) ---------------------------
@@ -2059,36 +2068,47 @@ static int sm_count() {
     return v;
 }
 
-// Per-device history of the warp-specialised hybrid's fallback rate.  Every CTA of
-// that kernel adds its pair and fallback counts to two cumulative device counters
-// and CTA 0 copies them to host-mapped memory (two posted writes at the end of
-// the kernel: no stream operation, no synchronisation); a launch reads
-// whatever has landed and, once at least 2^16
-// more pairs are accounted for, refreshes the rate.  A rate above TC_WS_SELF_RATE
-// selects the kernel instance whose iterative warps serve their own open
-// pairs when the ring is nearly full (TC_WS_SELF) -- the first launches of a
-// process, and launches after a change of workload, run the plain instance.
-#ifndef TC_WS_SELF_RATE
-#define TC_WS_SELF_RATE 0.6
+// Per-device history of the warp-specialised hybrid: is its fallback warpgroup
+// keeping up?  Every CTA of that kernel adds to four cumulative device counters
+// -- pairs, fallbacks, polls of iterative lanes on a full ring, tiles an
+// iterative warp served itself -- and CTA 0 copies them to host-mapped memory
+// (posted writes at the end of the kernel: no stream operation, no
+// synchronisation).  A launch reads whatever has landed and, once at least 2^16
+// more pairs are accounted for, decides which instance the next launches get:
+// the plain one switches to the self-serving one (TC_WS_SELF) when producers
+// polled a full ring more than TC_WS_SELF_ON times per tile, the self-serving one
+// back when fewer than TC_WS_SELF_OFF of its tiles were served that way.
+// Measured (2^24 pairs of the cfg1 generator, fp64): separation U[-0.1, 0.5]
+// (cfg1) 0.01 polls per tile, plain 2.024 ms / self-serving 2.054; U[0.05, 0.5]
+// 1.9 polls, 2.271 / 2.185; U[0.1, 0.5] 2.6 polls, 2.347 / 2.232; cfg3's
+// near-parallel class 706 polls, 0.365 / 0.259 ms per 2^20 pairs; its edge-edge
+// class 0.5 polls, 0.169 / 0.176.  The first launches of a process, and the
+// launches right after a change of workload, run the previous choice.
+#ifndef TC_WS_SELF_ON
+#define TC_WS_SELF_ON 1.0
+#endif
+#ifndef TC_WS_SELF_OFF
+#define TC_WS_SELF_OFF 0.01
 #endif
 struct FallbackHistory {
-    unsigned long long* counters = nullptr;      // host-mapped {pairs, fallbacks}
+    unsigned long long* counters = nullptr;      // host-mapped copy {pairs, fallbacks, ring polls, self-served tiles}
     unsigned long long* dev_counters = nullptr;  // the kernels' cumulative counters (device memory)
-    std::atomic<unsigned long long> seen_pairs{0}, seen_fb{0};
-    std::atomic<int> is_high{0};
+    std::mutex mu;
+    unsigned long long seen[4] = {0, 0, 0, 0};
+    int self_on = 0;
     std::once_flag once;
     bool high() {
         if (!dev_counters) return false;
-        const unsigned long long p = ((volatile unsigned long long*)counters)[0];
-        const unsigned long long f = ((volatile unsigned long long*)counters)[1];
-        const unsigned long long p0 = seen_pairs.load(std::memory_order_relaxed);
-        const unsigned long long f0 = seen_fb.load(std::memory_order_relaxed);
-        if (p >= p0 + 65536 && f >= f0) {
-            is_high.store((double)(f - f0) > TC_WS_SELF_RATE * (double)(p - p0), std::memory_order_relaxed);
-            seen_pairs.store(p, std::memory_order_relaxed);
-            seen_fb.store(f, std::memory_order_relaxed);
+        std::lock_guard<std::mutex> lk(mu);
+        unsigned long long c[4];
+        for (int k = 0; k < 4; ++k) c[k] = ((volatile unsigned long long*)counters)[k];
+        if (c[0] >= seen[0] + 65536 && c[2] >= seen[2] && c[3] >= seen[3]) {
+            const double tiles = (double)(c[0] - seen[0]) / 32.0;
+            if (!self_on) self_on = (double)(c[2] - seen[2]) > TC_WS_SELF_ON * tiles;
+            else self_on = (double)(c[3] - seen[3]) >= TC_WS_SELF_OFF * tiles;
+            for (int k = 0; k < 4; ++k) seen[k] = c[k];
         }
-        return is_high.load(std::memory_order_relaxed) != 0;
+        return self_on != 0;
     }
 };
 static FallbackHistory& fallback_history() {
@@ -2096,11 +2116,11 @@ static FallbackHistory& fallback_history() {
     FallbackHistory& h = hist[current_device()];
     std::call_once(h.once, [&h] {
         void *p = nullptr, *d = nullptr;
-        if (cudaHostAlloc(&p, 2 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) ==
+        if (cudaHostAlloc(&p, 4 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) ==
                 cudaSuccess &&
-            cudaMalloc(&d, 2 * sizeof(unsigned long long)) == cudaSuccess &&
-            cudaMemset(d, 0, 2 * sizeof(unsigned long long)) == cudaSuccess) {
-            memset(p, 0, 2 * sizeof(unsigned long long));
+            cudaMalloc(&d, 4 * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMemset(d, 0, 4 * sizeof(unsigned long long)) == cudaSuccess) {
+            memset(p, 0, 4 * sizeof(unsigned long long));
             h.counters = static_cast<unsigned long long*>(p);
             h.dev_counters = static_cast<unsigned long long*>(d);
         } else {
@@ -2176,7 +2196,7 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         FallbackHistory& fh = fallback_history();
         const bool self = TC_WS_SELF == 2 || (TC_WS_SELF == 1 && fh.high());
         Args<T> aw = a;
-        aw.hist = TC_WS_SELF == 1 ? fh.dev_counters : nullptr;
+        aw.hist = TC_WS_SELF >= 1 ? fh.dev_counters : nullptr;
         aw.hist_host = fh.counters;
         const Args<T>& a = aw;
         auto k = full ? (self ? hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, true, true>
@@ -2992,6 +3012,10 @@ int tc_allreduce_stats(tc_stats* stats, void* nccl_comm, void* stream) {
 }
 
 void tc_debug_set_max_ctas(int64_t max_ctas) { tc::g_max_ctas.store(max_ctas > 0 ? max_ctas : 0); }
+void tc_debug_fallback_history(uint64_t out[4]) {
+    tc::FallbackHistory& h = tc::fallback_history();
+    for (int k = 0; k < 4; ++k) out[k] = h.counters ? ((volatile unsigned long long*)h.counters)[k] : 0;
+}
 int tc_debug_fallback_rate_high(void) { return TC_WS_SELF == 1 && tc::fallback_history().high() ? 1 : 0; }
 
 void* tc_host_alloc(int64_t bytes) { return tc::host_alloc(bytes); }

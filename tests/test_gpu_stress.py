@@ -63,8 +63,9 @@ def test_release_determinism_and_cap_invariance(strict):
 def test_self_serving_instance_equals_plain(dtype):
     """The fast hybrid's self-serving instance (iterative warps run the comparison
     phases for their own open pairs when the ring is nearly full) is selected from
-    the device's fallback history: a batch with ~84 % fallbacks (cfg3 near-parallel
-    faces) switches it on, ordinary cfg1 pairs switch it off again, and every
+    the device's fallback history (polls of producers on a full ring switch it on,
+    no self-served tiles switch it off): a batch with ~84 % fallbacks (cfg3
+    near-parallel faces) switches it on, well-separated pairs off again, and every
     column, the ids and the counters equal the plain instance's bit for bit -- with
     and without feature ids, per-pair halos and an allow mask."""
     lib = _abi.load()

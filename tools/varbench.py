@@ -22,13 +22,14 @@ ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--strict", action="store_true")
 ap.add_argument("--variant", default="hybrid")
 ap.add_argument("--no-fallback", action="store_true", help="hybrid with an all-zero allow mask")
+ap.add_argument("--sep", type=float, nargs=2, default=(-0.1, 0.5), help="separation range of the cfg1 generator")
 ap.add_argument("--cfg3", type=int, default=-1, help="time class k (0-3) of the adversarial set, 2^20 pairs, instead of cfg1")
 args = ap.parse_args()
 dt = torch.float64 if args.dtype == "f64" else torch.float32
 n = args.n
 planes = torch.empty((18, n), dtype=torch.float64, device="cuda")
 lib0 = _abi.load()
-_abi.check(lib0.tc_random_pairs_soa_f64(0, 0, n, -0.1, 0.5, ctypes.c_void_p(planes.data_ptr()), None), "gen")
+_abi.check(lib0.tc_random_pairs_soa_f64(0, 0, n, args.sep[0], args.sep[1], ctypes.c_void_p(planes.data_ptr()), None), "gen")
 if args.cfg3 >= 0:
     n = 1 << 20
     A3, B3 = W.adversarial_pairs(n)
@@ -47,6 +48,7 @@ libs = [(Path(x).name, _abi.load(x)) for x in args.libs]
 ptr = lambda t: ctypes.c_void_p(t.data_ptr())
 cols = [ptr(out[k]) for k in ("distance", "point_a", "point_b", "bary_a", "bary_b", "kind")]
 res = {name: [] for name, _ in libs}
+hist_of, hist_txt = {}, {}
 stats_of = {}
 for r in range(args.rounds):
     for name, lib in libs:
@@ -69,8 +71,17 @@ for r in range(args.rounds):
         e1.record()
         torch.cuda.synchronize()
         res[name].append(e0.elapsed_time(e1) / args.reps)
+        if hasattr(lib, "tc_debug_fallback_history"):
+            h = (ctypes.c_uint64 * 4)()
+            lib.tc_debug_fallback_history(h)
+            prev = hist_of.get(name, [0, 0, 0, 0])
+            d = [int(h[k]) - prev[k] for k in range(4)]
+            hist_of[name] = [int(h[k]) for k in range(4)]
+            if d[0]:
+                hist_txt[name] = (f"history: fb/pair {d[1] / d[0]:.3f} ring waits/tile {32 * d[2] / d[0]:.2f} "
+                                  f"self tiles/tile {32 * d[3] / d[0]:.3f}")
         stats_of[name] = D.read_stats(stats)
 for name, ts in res.items():
     st = stats_of.get(name, {"fallback": 0, "contacts": 0})
     print(f"{name:40s} {min(ts):7.3f} ms  {n / min(ts) / 1e6:8.1f} M pairs/s  (rounds {' '.join(f'{t:.3f}' for t in ts)})"
-          f"  fb {st['fallback'] // (args.reps + 0)} contacts {st['contacts'] // args.reps}", flush=True)
+          f"  fb {st['fallback'] // (args.reps + 0)} contacts {st['contacts'] // args.reps}  {hist_txt.get(name, '')}", flush=True)
