@@ -623,7 +623,7 @@ def pcie_probe(torch, dev, mb=512, reps=5):
 def configs_table(D, torch, dev):
     """The other BASELINE.json configs on this GPU: cfg2 (all-pairs particle
     blocks, full 2,048-particle scene) and cfg3 (adversarial set, per class)."""
-    from paper_2105_12415_b200 import particles as PT, workloads as W
+    from paper_2105_12415_b200 import _abi, particles as PT, workloads as W
     res = {}
     meshes, blocks, gaps = PT.cfg2_scene()
     tm = torch.from_numpy(meshes).to(dev)
@@ -653,16 +653,23 @@ def configs_table(D, torch, dev):
         sl = slice(c << 20, (c + 1) << 20)
         planes = torch.from_numpy(W.to_soa(A[sl], B[sl])).to(dev)
         st = D.new_stats(dev)
-        D.run("hybrid", planes[:9], planes[9:], P, soa=True, out={}, n=1 << 20)
+        # steady state of the class: the library picks the hybrid's kernel instance from what
+        # the previous launches on the device measured (tc_debug_fallback_rate_high)
+        for _ in range(3):
+            D.run("hybrid", planes[:9], planes[9:], P, soa=True, out={}, n=1 << 20)
+            torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
         e0.record()
-        D.run("hybrid", planes[:9], planes[9:], P, soa=True, stats=st, n=1 << 20)
+        for _ in range(reps):
+            D.run("hybrid", planes[:9], planes[9:], P, soa=True, stats=st, n=1 << 20)
         e1.record()
         torch.cuda.synchronize()
         s = D.read_stats(st)
-        c3[name] = {"pairs": 1 << 20, "pairs_per_s": (1 << 20) / (e0.elapsed_time(e1) / 1e3),
-                    "fallback_rate": s["fallback"] / (1 << 20), "degenerate": s["degenerate"],
-                    "contacts": s["contacts"]}
+        c3[name] = {"pairs": 1 << 20, "pairs_per_s": reps * (1 << 20) / (e0.elapsed_time(e1) / 1e3),
+                    "fallback_rate": s["fallback"] / reps / (1 << 20), "degenerate": s["degenerate"] // reps,
+                    "contacts": s["contacts"] // reps,
+                    "self_serving_instance": bool(_abi.load().tc_debug_fallback_rate_high())}
     res["cfg3_fast"] = c3
     res["multiscale"] = multiscale_table(D, torch, dev)
     res["note"] = ("oracle agreement of cfg2/cfg3: tests/test_gpu_blocks.py, tests/test_gpu_cfg3.py "

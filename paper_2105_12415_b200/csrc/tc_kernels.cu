@@ -1250,6 +1250,9 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
                     }
                     if (d == WS_IW) break;  // all produced and claimed
                     __nanosleep(256);
+#ifdef TC_X_COUNT_FB_IDLE  // experiment: the leader's idle polls in place of the self-served tiles
+                    atomicAdd(&S.self_tiles, 1u);
+#endif
                 }
                 G.m = m;
                 G.pos = h;
