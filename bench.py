@@ -655,14 +655,15 @@ def configs_table(D, torch, dev):
         st = D.new_stats(dev)
         # steady state of the class: the library picks the hybrid's kernel instance from what
         # the previous launches on the device measured (tc_debug_fallback_rate_high)
+        out = D.alloc_outputs(1 << 20, planes.dtype, dev, soa=True)
         for _ in range(3):
-            D.run("hybrid", planes[:9], planes[9:], P, soa=True, out={}, n=1 << 20)
+            D.run("hybrid", planes[:9], planes[9:], P, soa=True, out=out, n=1 << 20)
             torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 3
+        reps = 10  # back to back, so the ~0.2 ms kernels hide the launch calls
         e0.record()
         for _ in range(reps):
-            D.run("hybrid", planes[:9], planes[9:], P, soa=True, stats=st, n=1 << 20)
+            D.run("hybrid", planes[:9], planes[9:], P, soa=True, out=out, stats=st, n=1 << 20)
         e1.record()
         torch.cuda.synchronize()
         s = D.read_stats(st)

@@ -119,12 +119,12 @@ def main():
     lib = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "paper_2105_12415_b200", "libtricontact_b200.so")
     sp = spans()
     chains = line_chains(lib, mangled)
-    m = re.match(r"(\w+?)I([df])Lb([01])ELb([01])E?(?:Li(\d+)ELi(\d+)E)?(?:Lb([01])E)?", mangled)
+    m = re.match(r"(\w+?)I([df])Lb([01])ELb([01])E?(?:Li(\d+)ELi(\d+)E)?((?:Lb[01]E)*)", mangled)
     ksub = mangled
     if m:
         ksub = f"{m.group(1)}<{'double' if m.group(2) == 'd' else 'float'}, (bool){m.group(3)}, (bool){m.group(4)}"
         if m.group(5):
-            ksub += f", (int){m.group(5)}, (int){m.group(6)}" + (f", (bool){m.group(7)}>" if m.group(7) else ">")
+            ksub += f", (int){m.group(5)}, (int){m.group(6)}" + "".join(f", (bool){b}" for b in re.findall(r"Lb([01])E", m.group(7) or "")) + ">"
         else:
             ksub += ">"
     rows = sass_rows(rep, ksub)
