@@ -64,6 +64,7 @@ SIGNATURES = {
     "tc_host_alloc": (_P, [_I64]),
     "tc_debug_set_max_ctas": (None, [_I64]),
     "tc_debug_fallback_rate_high": (_INT, []),
+    "tc_debug_hybrid_mode": (_INT, []),
     "tc_debug_fallback_history": (None, [_P]),
     "tc_host_free": (_INT, [_P]),
     "tc_random_pairs_soa_f64": (_INT, [ctypes.c_uint64, _I64, _I64, ctypes.c_double, ctypes.c_double, _P, _P]),

@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(BS_HYB, sizeof(T) == 4 ? TC_HYB_CTAS_F32 : TC_
     }
     if (TC_TILE_CPASYNC) cp_async_wait_all();
     drain<true, R>(FlatSource<SOA, R, T, BS_HYB>{a, slot}, Q, tl, true, (uint32_t)FLAG_FALLBACK);
-    tl.flush<true>(a.stats);
+    tl.flush<true, BS_HYB / 32>(a.stats, a.hist, a.hist_host);  // (the history: pairs and fallbacks)
 }
 
 
@@ -2093,26 +2093,47 @@ static int sm_count() {
 #ifndef TC_WS_SELF_OFF
 #define TC_WS_SELF_OFF 0.01
 #endif
+// With few fallbacks the warpgroup that waits for them is a quarter of the SM
+// idle: the fused kernel, whose 16 warps all iterate, is 4 % faster (2^24 far
+// pairs, 0.1-3 % fallbacks: 1.59-1.71 ms against 1.52-1.65; at no fallbacks
+// 1.678 / 1.547; the lines cross near 17 %).  Below TC_WS_FUSED_BELOW
+// fallbacks per pair the next launches use it, above TC_WS_FUSED_ABOVE the
+// warp-specialised kernel again.
+#ifndef TC_WS_FUSED_BELOW
+#define TC_WS_FUSED_BELOW 0.08
+#endif
+#ifndef TC_WS_FUSED_ABOVE
+#define TC_WS_FUSED_ABOVE 0.12
+#endif
 struct FallbackHistory {
+    enum Mode { PLAIN = 0, SELF = 1, FUSED = 2 };
     unsigned long long* counters = nullptr;      // host-mapped copy {pairs, fallbacks, ring polls, self-served tiles}
     unsigned long long* dev_counters = nullptr;  // the kernels' cumulative counters (device memory)
     std::mutex mu;
     unsigned long long seen[4] = {0, 0, 0, 0};
-    int self_on = 0;
+    int cur = PLAIN;
     std::once_flag once;
-    bool high() {
-        if (!dev_counters) return false;
+    int mode() {
+        if (!dev_counters) return PLAIN;
         std::lock_guard<std::mutex> lk(mu);
         unsigned long long c[4];
         for (int k = 0; k < 4; ++k) c[k] = ((volatile unsigned long long*)counters)[k];
-        if (c[0] >= seen[0] + 65536 && c[2] >= seen[2] && c[3] >= seen[3]) {
-            const double tiles = (double)(c[0] - seen[0]) / 32.0;
-            if (!self_on) self_on = (double)(c[2] - seen[2]) > TC_WS_SELF_ON * tiles;
-            else self_on = (double)(c[3] - seen[3]) >= TC_WS_SELF_OFF * tiles;
+        if (c[0] >= seen[0] + 65536 && c[1] >= seen[1] && c[2] >= seen[2] && c[3] >= seen[3]) {
+            const double pairs = (double)(c[0] - seen[0]), tiles = pairs / 32.0;
+            const double rate = (double)(c[1] - seen[1]) / pairs;
+            if (cur == PLAIN) {
+                if ((double)(c[2] - seen[2]) > TC_WS_SELF_ON * tiles) cur = SELF;
+                else if (rate < TC_WS_FUSED_BELOW) cur = FUSED;
+            } else if (cur == SELF) {
+                if ((double)(c[3] - seen[3]) < TC_WS_SELF_OFF * tiles) cur = PLAIN;
+            } else if (rate > TC_WS_FUSED_ABOVE) {
+                cur = PLAIN;
+            }
             for (int k = 0; k < 4; ++k) seen[k] = c[k];
         }
-        return self_on != 0;
+        return cur;
     }
+    bool high() { return mode() == SELF; }
 };
 static FallbackHistory& fallback_history() {
     static FallbackHistory hist[kMaxDevices];
@@ -2189,37 +2210,53 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         const int64_t cap = g_max_ctas.load(std::memory_order_relaxed);  // test knob
         if (cap > 0 && g > cap) g = cap;
         k<<<(unsigned)g, 32 * (IW + FW), smem, s>>>(a);
-    } else if constexpr (TC_HYBRID_WS && (!STRICT || TC_WS_STRICT) && (sizeof(T) == 8 ? TC_WS_IW_F64 : TC_WS_IW_F32) > 0) {
-        // warp-specialised hybrid: one CTA per SM
-        constexpr int IW = sizeof(T) == 8 ? TC_WS_IW_F64 : (TC_WS_IW_F32 > 0 ? TC_WS_IW_F32 : 1);
-        constexpr int FWG = sizeof(T) == 8 ? TC_WS_FWG_F64 : TC_WS_FWG_F32;
-        // the full-record instance (every column, no ids) has no per-column null tests
-        const bool full = TC_WS_FULL && full_record(a);
-        // the self-serving instance when this device's recent launches fell back a lot (fallback_history)
-        FallbackHistory& fh = fallback_history();
-        const bool self = TC_WS_SELF == 2 || (TC_WS_SELF == 1 && fh.high());
-        Args<T> aw = a;
-        aw.hist = TC_WS_SELF >= 1 ? fh.dev_counters : nullptr;
-        aw.hist_host = fh.counters;
-        const Args<T>& a = aw;
-        auto k = full ? (self ? hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, true, true>
-                              : hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, true, false>)
-                      : (self ? hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, false, true>
-                              : hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, false, false>);
-        const size_t smem = ws_smem_bytes<T, IW, FWG>(self);
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int64_t ctas = (a.n + 32 * IW - 1) / (32 * IW);
-        int64_t g = ctas < sm_count() ? ctas : sm_count();
-        const int64_t cap = g_max_ctas.load(std::memory_order_relaxed);  // test knob
-        if (cap > 0 && g > cap) g = cap;
-        k<<<(unsigned)g, 32 * IW + FWG * WS_FB, smem, s>>>(a);
     } else {
-        auto k = hybrid_kernel<T, STRICT, SOA>;
+        constexpr bool WS = TC_HYBRID_WS && (!STRICT || TC_WS_STRICT) &&
+                            (sizeof(T) == 8 ? TC_WS_IW_F64 : TC_WS_IW_F32) > 0;
+        Args<T> aw = a;
+        int mode = FallbackHistory::PLAIN;
+        if constexpr (WS) {
+            // which kernel this device's recent fast hybrid launches ask for (fallback_history)
+            if (TC_WS_SELF >= 1) {
+                FallbackHistory& fh = fallback_history();
+                aw.hist = fh.dev_counters;
+                aw.hist_host = fh.counters;
+                mode = TC_WS_SELF == 2 ? (int)FallbackHistory::SELF : fh.mode();
+            }
+        }
+        bool launched = false;
+        if constexpr (WS) {
+            if (mode != FallbackHistory::FUSED) {
+                // warp-specialised hybrid: one CTA per SM
+                constexpr int IW = sizeof(T) == 8 ? TC_WS_IW_F64 : (TC_WS_IW_F32 > 0 ? TC_WS_IW_F32 : 1);
+                constexpr int FWG = sizeof(T) == 8 ? TC_WS_FWG_F64 : TC_WS_FWG_F32;
+                // the full-record instance (every column, no ids) has no per-column null tests
+                const bool full = TC_WS_FULL && full_record(aw);
+                const bool self = mode == FallbackHistory::SELF;
+                auto k = full ? (self ? hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, true, true>
+                                      : hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, true, false>)
+                              : (self ? hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, false, true>
+                                      : hybrid_ws_kernel<T, STRICT, SOA, IW, FWG, false, false>);
+                const size_t smem = ws_smem_bytes<T, IW, FWG>(self);
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                const int64_t ctas = (aw.n + 32 * IW - 1) / (32 * IW);
+                int64_t g = ctas < sm_count() ? ctas : sm_count();
+                const int64_t cap = g_max_ctas.load(std::memory_order_relaxed);  // test knob
+                if (cap > 0 && g > cap) g = cap;
+                k<<<(unsigned)g, 32 * IW + FWG * WS_FB, smem, s>>>(aw);
+                launched = true;
+            }
+        }
+        if (!launched) {
+            // the fused kernel: strict builds, and fast batches with few fallbacks
+            auto k = hybrid_kernel<T, STRICT, SOA>;
 #ifndef TC_X_PAD
 #define TC_X_PAD 0
 #endif
-        const size_t smem = scratch_bytes<T>(BS_HYB) + (TC_TILE_CPASYNC ? sizeof(T) * SLOT * BS_HYB : 0) + TC_X_PAD;
-        k<<<(unsigned)grid_for(k, a.n, smem, BS_HYB), BS_HYB, smem, s>>>(a);
+            const size_t smem =
+                scratch_bytes<T>(BS_HYB) + (TC_TILE_CPASYNC ? sizeof(T) * SLOT * BS_HYB : 0) + TC_X_PAD;
+            k<<<(unsigned)grid_for(k, aw.n, smem, BS_HYB), BS_HYB, smem, s>>>(aw);
+        }
     }
     g_launches++;
     const cudaError_t e = cudaGetLastError();
@@ -3020,6 +3057,7 @@ void tc_debug_fallback_history(uint64_t out[4]) {
     for (int k = 0; k < 4; ++k) out[k] = h.counters ? ((volatile unsigned long long*)h.counters)[k] : 0;
 }
 int tc_debug_fallback_rate_high(void) { return TC_WS_SELF == 1 && tc::fallback_history().high() ? 1 : 0; }
+int tc_debug_hybrid_mode(void) { return TC_WS_SELF == 1 ? tc::fallback_history().mode() : 0; }
 
 void* tc_host_alloc(int64_t bytes) { return tc::host_alloc(bytes); }
 int tc_host_free(void* p) { return tc::host_free(p); }

@@ -429,25 +429,26 @@ struct Scratch {
 template <class R, class Tri>
 __device__ __forceinline__ void inside_point_params(const R* p, const Tri& tri, R& u, R& w) {
     using T = typename Store<R>::type;
+    // (pinned operations, tc_math.cuh: the same bits in every inlining context)
     R a[3], ab[3], ac[3], ap[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         a[i] = tri[i];
-        ab[i] = tri[3 + i] - a[i];
-        ac[i] = tri[6 + i] - a[i];
-        ap[i] = p[i] - a[i];
+        ab[i] = subp(tri[3 + i], a[i]);
+        ac[i] = subp(tri[6 + i], a[i]);
+        ap[i] = subp(p[i], a[i]);
     }
-    const R uu = dot3(ab, ab), uv = dot3(ab, ac), vv = dot3(ac, ac);
-    const R det = uu * vv - uv * uv;
+    const R uu = dot3p(ab, ab), uv = dot3p(ab, ac), vv = dot3p(ac, ac);
+    const R det = fmav(uu, vv, -mulp(uv, uv));
     const R kappa = R(T(sizeof(T) == 8 ? 1e-6 : 1e-2));
-    if (!(det >= kappa * (uu * vv)) || det == R(0)) {
+    if (!(det >= mulp(kappa, mulp(uu, vv))) || det == R(0)) {
         closest_point_params_t(p, tri, u, w);
         return;
     }
     const R r = rcpv(det);
-    const R pu = dot3(ap, ab), pv = dot3(ap, ac);
-    u = (vv * pu - uv * pv) * r;
-    w = (uu * pv - uv * pu) * r;
+    const R pu = dot3p(ap, ab), pv = dot3p(ap, ac);
+    u = mulp(fmav(vv, pu, -mulp(uv, pv)), r);
+    w = mulp(fmav(uu, pv, -mulp(uv, pu)), r);
 }
 
 template <class R, class Tri>

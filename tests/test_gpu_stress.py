@@ -71,7 +71,12 @@ def test_self_serving_instance_equals_plain(dtype):
     lib = _abi.load()
     n = 1 << 17
     A3, B3 = W.adversarial_pairs(n)
-    hot = torch.from_numpy(W.to_soa(A3[:n], B3[:n])).cuda().to(dtype)  # class 0: near-parallel
+    # class 0 (near-parallel faces, ~84 % fallbacks, few intersections) mixed with cfg1 pairs
+    # (41 % fallbacks, most of them intersecting): both fallback outcomes get self-served
+    Ac, Bc = W.random_pairs(n // 8, seed=47, sep=(-0.1, 0.5))
+    perm = np.random.default_rng(7).permutation(n + n // 8)[:n]
+    Ah, Bh = np.concatenate([A3[:n], Ac])[perm], np.concatenate([B3[:n], Bc])[perm]
+    hot = torch.from_numpy(W.to_soa(Ah, Bh)).cuda().to(dtype)
     A1, B1 = W.random_pairs(n, seed=43, sep=(0.3, 0.5))  # well separated: few fallbacks
     cold = torch.from_numpy(W.to_soa(A1, B1)).cuda().to(dtype)
     P = D.Params(n_iterative=16, epsilon=1e-6)
@@ -104,8 +109,47 @@ def test_self_serving_instance_equals_plain(dtype):
     plain += [run(hot, ids=True), ]            # plain again (the launch reads the history first)
     settle(cold, 0)
     plain += [run(hot, ids=True, eps=eps, allow=allow)]
-    assert served[0]["stats"][2] > 0.7 * n     # the batch does fall back
+    assert served[0]["stats"][2] > 0.6 * n     # the batch does fall back
+    assert served[0]["stats"][5] > 0.02 * n    # ... and has intersecting pairs
     for a, b in zip(plain, served):
         assert a.keys() == b.keys()
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+
+
+def test_fused_kernel_for_rare_fallbacks_equals_warp_specialised():
+    """Far-apart pairs (under 8 % fallbacks) switch the fast hybrid to the fused kernel,
+    ordinary pairs back; both kernels give the same bits."""
+    lib = _abi.load()
+    n = 1 << 17
+    Af, Bf = W.random_pairs(n, seed=51, sep=(2.0, 3.0))
+    far = torch.from_numpy(W.to_soa(Af, Bf)).cuda()
+    Ac, Bc = W.random_pairs(n, seed=53, sep=(-0.1, 0.5))
+    near = torch.from_numpy(W.to_soa(Ac, Bc)).cuda()
+    P = D.Params(n_iterative=16, epsilon=1e-6)
+
+    def run(pl, **kw):
+        st = D.new_stats()
+        out = D.run("hybrid", pl[:9], pl[9:], P, soa=True, stats=st, **kw)
+        torch.cuda.synchronize()
+        res = {k: v.cpu().numpy() for k, v in out.items()}
+        res["stats"] = np.array(list(D.read_stats(st).values()))
+        return res
+
+    def settle(pl, want):
+        for _ in range(8):
+            run(pl)
+            if lib.tc_debug_hybrid_mode() == want:
+                return
+        raise AssertionError(f"hybrid mode did not reach {want}")
+
+    settle(near, 0)
+    ws = [run(far, ids=True), ]
+    settle(far, 2)
+    fused = [run(far, ids=True), run(near, ids=True)]
+    settle(near, 0)
+    ws += [run(near, ids=True)]
+    assert ws[0]["stats"][2] < 0.05 * n
+    for a, b in zip(ws, fused):
         for k in a:
             assert np.array_equal(a[k], b[k]), k
