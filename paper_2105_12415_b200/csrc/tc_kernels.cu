@@ -2217,7 +2217,14 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
         int mode = FallbackHistory::PLAIN;
         if constexpr (WS) {
             // which kernel this device's recent fast hybrid launches ask for (fallback_history)
-            if (TC_WS_SELF >= 1) {
+            // (not while the caller captures a graph: the history's first use allocates, and a
+            // captured launch would freeze one choice anyway -- it gets the plain instance)
+            cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+            if (cudaStreamIsCapturing(s, &cap_status) != cudaSuccess) {
+                cudaGetLastError();
+                cap_status = cudaStreamCaptureStatusNone;
+            }
+            if (TC_WS_SELF >= 1 && cap_status == cudaStreamCaptureStatusNone) {
                 FallbackHistory& fh = fallback_history();
                 aw.hist = fh.dev_counters;
                 aw.hist_host = fh.counters;

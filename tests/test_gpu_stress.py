@@ -153,3 +153,30 @@ def test_fused_kernel_for_rare_fallbacks_equals_warp_specialised():
     for a, b in zip(ws, fused):
         for k in a:
             assert np.array_equal(a[k], b[k]), k
+
+
+def test_fast_hybrid_under_graph_capture():
+    """A caller may capture the launch in a CUDA graph: the library then leaves its
+    per-device history alone (no allocation, no choice frozen from it) and the
+    replayed kernel gives the eager results."""
+    n = 1 << 15
+    A, B = W.random_pairs(n, seed=61, sep=(-0.1, 0.5))
+    pl = torch.from_numpy(W.to_soa(A, B)).cuda()
+    P = D.Params(n_iterative=16, epsilon=1e-6)
+    eager = D.run("hybrid", pl[:9], pl[9:], P, soa=True)
+    torch.cuda.synchronize()
+    out = D.alloc_outputs(n, pl.dtype, "cuda", soa=True)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        D.run("hybrid", pl[:9], pl[9:], P, soa=True, out=out)  # warm-up outside the capture
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        D.run("hybrid", pl[:9], pl[9:], P, soa=True, out=out)
+    for v in out.values():
+        v.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for k in eager:
+        assert torch.equal(eager[k], out[k]), k
