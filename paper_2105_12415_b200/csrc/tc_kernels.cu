@@ -900,7 +900,21 @@ constexpr int WS_RING = TC_WS_RING;  // ring slots (256: 2.347 ms -- producers w
 #endif
 constexpr int WS_FB = TC_WS_FB;      // threads of one fallback warpgroup (= one batch)
 constexpr int WS_Q2 = TC_WS_Q2 < 2 * WS_FB ? TC_WS_Q2 : 2 * WS_FB;      // phase-2 stack entries per warpgroup (< 2 WS_FB: phase-1 batches shrink to fit)
-constexpr int WS_NBUF = TC_WS_ASYNC ? 2 : 1;  // stash buffers per iterative warp
+// TC_WS_ASYNC_LANE_F32 / _F64: the same double buffering with every lane copying its own pair
+// (18 element-sized cp.async into its stash slots, any layout, alignment or tile tail; no warp
+// synchronisation: a lane only ever reads its own slots).  With the paired fp32 stash the fp32
+// hybrid gains 2.8 % (1.235 -> 1.200 ms, bitwise equal); fp64 does not have the shared memory for
+// a second stash next to the full ring, and loses with a smaller one: on for float only.
+#ifndef TC_WS_ASYNC_LANE_F32
+#define TC_WS_ASYNC_LANE_F32 1
+#endif
+#ifndef TC_WS_ASYNC_LANE_F64
+#define TC_WS_ASYNC_LANE_F64 0
+#endif
+template <typename T>
+__host__ __device__ constexpr bool ws_async_lane() { return sizeof(T) == 8 ? TC_WS_ASYNC_LANE_F64 : TC_WS_ASYNC_LANE_F32; }
+template <typename T>
+__host__ __device__ constexpr int ws_nbuf() { return (TC_WS_ASYNC || ws_async_lane<T>()) ? 2 : 1; }  // stash buffers per iterative warp
 static_assert(WS_Q2 >= WS_FB + 32 && WS_Q2 <= 2 * WS_FB, "phase-2 stack size");
 
 constexpr int64_t WS_FREE = -1;
@@ -941,7 +955,7 @@ struct WsShared {
 // [iterative stash 18 x 32 IW]
 template <typename T, int IW, int FWG>
 constexpr size_t ws_smem_bytes(bool self) {
-    return sizeof(T) * (18 * WS_RING + FWG * (18 * WS_Q2 + SCR * WS_FB) + WS_NBUF * 18 * 32 * IW +
+    return sizeof(T) * (18 * WS_RING + FWG * (18 * WS_Q2 + SCR * WS_FB) + ws_nbuf<T>() * 18 * 32 * IW +
                         (self ? SCR * 32 * IW : 0));
 }
 // Producer / consumer ordering inside the CTA.  TC_WS_FENCE 1: fence.acq_rel.cta
@@ -1028,7 +1042,9 @@ template <typename T, bool STRICT, bool SOA, int WS_IW, int WS_FWG, bool FULL, b
 __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kernel(const __grid_constant__ Args<T> a) {
     using R = typename Pol<T, STRICT>::R;
     constexpr bool PAIRED = sizeof(T) == 8 ? TC_WS_PAIRED_F64 : TC_WS_PAIRED_F32;
-    static_assert(!(TC_WS_ASYNC && PAIRED), "the cp.async tiles land in planar layout");
+    static_assert(!(TC_WS_ASYNC && PAIRED), "the 16-byte cp.async tiles land in planar layout");
+    constexpr bool LANE_ASYNC = ws_async_lane<T>() && !TC_WS_ASYNC;
+    constexpr int WS_NBUF = ws_nbuf<T>();
     constexpr int WS_IT = 32 * WS_IW;  // iterative threads
     constexpr int WS_BS = WS_IT + WS_FWG * WS_FB;
     __shared__ WsShared<WS_FWG> S;
@@ -1076,9 +1092,25 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
+        // LANE_ASYNC: lane-wise copy of pair wt * 32 + lane into the lane's slots of `buf`
+        auto issue_lane = [&](int64_t wt, T* buf) {
+            const int64_t j = wt * 32 + lane;
+            if (wt < nwt && j < a.n) {
+#pragma unroll
+                for (int c = 0; c < 18; ++c) {
+                    const T* src = SOA ? (c < 9 ? a.tri_a + (int64_t)c * a.n : a.tri_b + (int64_t)(c - 9) * a.n) + j
+                                       : (c < 9 ? a.tri_a + 9 * j + c : a.tri_b + 9 * j + (c - 9));
+                    // coordinate c of this lane: planar slot[c * 32], paired word (c >> 1) * 32, half c & 1
+                    T* dst = PAIRED ? buf + ((c >> 1) * 32 + lane) * 2 + (c & 1) : buf + c * 32 + lane;
+                    cp_async_val(dst, src);
+                }
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
         int cur = 0;
         const int64_t wt0 = (int64_t)blockIdx.x * WS_IW + wid;
-        if (pre(wt0)) issue(wt0, wstash);
+        if (LANE_ASYNC) issue_lane(wt0, wstash);
+        else if (pre(wt0)) issue(wt0, wstash);
         for (int64_t wt = wt0; wt < nwt; wt += wstep) {
             const int64_t i = wt * 32 + lane;
             T* const slot = wstash + cur * (18 * 32) + lane;
@@ -1086,8 +1118,12 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
             // word kk * 32 + l): the stash, the epilogue's re-read and the ring copy move 16 bytes at a time
             using T2 = typename Vec2<T>::type;
             T2* const slot2 = reinterpret_cast<T2*>(wstash + cur * (18 * 32)) + lane;
-            const bool staged = pre(wt);
-            if (TC_WS_ASYNC) {
+            const bool staged = LANE_ASYNC || pre(wt);
+            if (LANE_ASYNC) {
+                cp_async_wait_all();  // (a lane reads only the slots it copied itself: no warp barrier)
+                cur ^= 1;
+                issue_lane(wt + wstep, wstash + cur * (18 * 32));
+            } else if (TC_WS_ASYNC) {
                 if (staged) cp_async_wait_all();
                 __syncwarp();  // the tile is visible to every lane; the previous tile's reads of the spare buffer are done
                 cur ^= 1;
@@ -1096,7 +1132,15 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
             bool enq = false;
             if (i < a.n) {
                 R A[9], B[9], eps;
-                if (staged) {
+                if (staged && PAIRED) {
+#pragma unroll
+                    for (int kk = 0; kk < 9; ++kk) {
+                        const T2 v = slot2[kk * 32];
+                        const int c = 2 * kk;
+                        (c < 9 ? A[c] : B[c - 9]) = R(v.x);
+                        (c + 1 < 9 ? A[c + 1] : B[c + 1 - 9]) = R(v.y);
+                    }
+                } else if (staged) {
 #pragma unroll
                     for (int k = 0; k < 9; ++k) {
                         A[k] = R(slot[k * 32]);
