@@ -363,14 +363,20 @@ struct Tally {
     // pairs); widened to 64 bits in the CTA reduction
     unsigned iterative = 0, comparison = 0, degenerate = 0, contacts = 0, intersecting = 0;
     double min_d = __builtin_huge_val();
+    float min_f = __builtin_huge_valf();  // fp32 kernels keep the running minimum in float (exact; no FP64 pipe)
 
     template <class R>
     __device__ __forceinline__ void result(const Rec<R>& r) {
         if (r.kind == KIND_DEGENERATE) return;
         contacts += (r.kind == KIND_CONTACT);
         intersecting += (r.ids >> 24) & FLAG_INTERSECT ? 1 : 0;
-        const double d = (double)val(r.distance) + 0.0;  // -0 -> +0
-        min_d = (d < min_d) ? d : min_d;
+        if constexpr (sizeof(typename Store<R>::type) == 4) {
+            const float d = (float)val(r.distance) + 0.0f;  // -0 -> +0
+            min_f = (d < min_f) ? d : min_f;
+        } else {
+            const double d = (double)val(r.distance) + 0.0;  // -0 -> +0
+            min_d = (d < min_d) ? d : min_d;
+        }
     }
 
     // COMPARISON_IS_FALLBACK: hybrid comparisons also count as fallbacks
@@ -381,6 +387,7 @@ struct Tally {
         __shared__ unsigned long long red[5][NWARPS];  // iterative, comparison, degenerate, contacts, intersecting
         __shared__ double redm[NWARPS];
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if ((double)min_f < min_d) min_d = (double)min_f;
         unsigned long long it64 = iterative, cm64 = comparison, dg64 = degenerate, ct64 = contacts,
                            ix64 = intersecting;
 #pragma unroll
