@@ -865,6 +865,11 @@ __global__ void __launch_bounds__(BS_HYB, sizeof(T) == 4 ? TC_HYB_CTAS_F32 : TC_
 // fp32 (80 registers): 16 + 8 warps (1.375 -> 1.290 ms; 12 + 8 1.390, 18 + 8
 // 1.325, 16 + 12 1.312).  Strict builds keep the fused kernel (with this one:
 // fp64 +3.3 %, fp32 +8.3 %; TC_WS_STRICT).
+// Template flags: FULL (every result column requested, no ids: no per-column
+// null tests), SELF (iterative warps serve their own open pairs when the ring
+// is nearly full: TC_WS_SELF, ws_self_serve).  Which of {this kernel, its SELF
+// instance, the fused kernel} a fast hybrid launch gets follows the device's
+// FallbackHistory (launch3); all three give the same bits.
 #ifndef TC_HYBRID_WS
 #define TC_HYBRID_WS 1
 #endif
