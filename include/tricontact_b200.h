@@ -283,8 +283,8 @@ void tc_debug_set_max_ctas(int64_t max_ctas);
  * not (tests/test_gpu_stress.py). */
 int tc_debug_fallback_rate_high(void);
 /* The kernel the next fast hybrid launch on the current device gets: 0 the
- * warp-specialised kernel, 1 its self-serving instance, 2 the fused kernel
- * (recent launches had few fallbacks). */
+ * warp-specialised kernel, 1 its self-serving instance, 2 the kernel for
+ * batches with few fallbacks (every warp iterates and serves its own queue). */
 int tc_debug_hybrid_mode(void);
 /* The history's cumulative counters as last published by a kernel: pairs,
  * fallbacks, ring waits of the iterative warps (per lane and poll), self-served tiles. */

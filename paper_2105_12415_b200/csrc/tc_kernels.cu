@@ -419,12 +419,20 @@ struct Tally {
                 if (ring_waits) atomicAdd(hist + 2, (unsigned long long)ring_waits);
                 if (self_tiles) atomicAdd(hist + 3, (unsigned long long)self_tiles);
                 if (blockIdx.x == 0) {
-                    // two posted writes to host memory per launch (per-CTA system-scope
+                    // a few posted writes to host memory per launch (per-CTA system-scope
                     // reductions over PCIe cost 0.2 ms per launch); the totals of CTAs
-                    // still running reach the host with the next launch
+                    // still running reach the host with the next launch.  The snapshot is
+                    // bracketed by a sequence number (words 0 and 5) so the host never
+                    // uses a torn one (a launch once read the new pair count with the old
+                    // fallback count, took the rate for 0 and switched kernels).
                     __threadfence();
-                    for (int k = 0; k < 4; ++k)
-                        ((volatile unsigned long long*)hist_host)[k] = ((volatile unsigned long long*)hist)[k];
+                    volatile unsigned long long* hh = hist_host;
+                    const unsigned long long seq = atomicAdd(hist + 4, 1ull) + 1ull;
+                    hh[0] = seq;
+                    __threadfence_system();
+                    for (int k = 0; k < 4; ++k) hh[1 + k] = ((volatile unsigned long long*)hist)[k];
+                    __threadfence_system();
+                    hh[5] = seq;
                 }
             }
             if (!s) return;
@@ -1390,6 +1398,112 @@ __global__ void __launch_bounds__(32 * WS_IW + WS_FWG * WS_FB, 1) hybrid_ws_kern
     tl.flush<true, WS_BS / 32>(a.stats, a.hist, a.hist_host, S.ring_waits, S.self_tiles);
 }
 
+// ---- hybrid for batches with few fallbacks (TC_WQ) ---------------------------------------
+// All 16 warps of the one CTA per SM iterate (lane-wise cp.async prefetch of the
+// next tile into a second stash buffer, as in hybrid_ws_kernel); a warp keeps the
+// indices of its open pairs in a private 64-entry queue and, once 32 have
+// gathered, serves them itself: every lane re-reads one queued pair from global
+// memory (L2) into its free stash slot and runs ws_self_serve on it.  No warp
+// waits for another, nobody idles while fallbacks are rare -- the regime the
+// fallback history sends here (under TC_WS_FUSED_BELOW fallbacks per pair).
+// At cfg1's 41 % the gathers and the divergence of warp-private batches lose
+// (round 1 measured -10 % for warp-private queues); results are the same bits.
+#ifndef TC_WQ
+#define TC_WQ 1
+#endif
+constexpr int WQ_WARPS = 16;
+constexpr int WQ_CAP = 64;
+template <typename T>
+constexpr size_t wq_smem_bytes() {
+    return sizeof(T) * (2 * 18 * 32 * WQ_WARPS + SCR * 32 * WQ_WARPS);
+}
+template <typename T, bool STRICT, bool SOA, bool FULL>
+__global__ void __launch_bounds__(32 * WQ_WARPS, 1) hybrid_wq_kernel(const __grid_constant__ Args<T> a) {
+    using R = typename Pol<T, STRICT>::R;
+    __shared__ int64_t queue[WQ_WARPS][WQ_CAP];
+    extern __shared__ __align__(16) unsigned char tc_dyn_smem[];
+    T* const base = reinterpret_cast<T*>(tc_dyn_smem);
+    Tally tl;
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const KP<R> kp = make_kp<R>(a);
+    T* const wstash = base + wid * (2 * 18 * 32);
+    T* const scr_p = base + 2 * 18 * 32 * WQ_WARPS + wid * (SCR * 32) + lane;
+    int64_t* const q = queue[wid];
+    int nq = 0;  // queued open pairs of this warp (warp-uniform)
+    const int64_t nwt = (a.n + 31) / 32;
+    const int64_t wstep = (int64_t)gridDim.x * WQ_WARPS;
+    auto issue_lane = [&](int64_t wt, T* buf) {
+        const int64_t j = wt * 32 + lane;
+        if (wt < nwt && j < a.n) {
+#pragma unroll
+            for (int c = 0; c < 18; ++c) {
+                const T* src = SOA ? (c < 9 ? a.tri_a + (int64_t)c * a.n : a.tri_b + (int64_t)(c - 9) * a.n) + j
+                                   : (c < 9 ? a.tri_a + 9 * j + c : a.tri_b + 9 * j + (c - 9));
+                cp_async_val(buf + c * 32 + lane, src);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // the comparison phases for up to 32 queued pairs, one per lane, staged in `slot`
+    auto serve = [&](int cnt, T* slot) {
+        const int64_t j = lane < cnt ? q[nq - cnt + lane] : -1;
+        nq -= cnt;
+        if (j >= 0) {
+#pragma unroll
+            for (int c = 0; c < 18; ++c)
+                slot[c * 32] = __ldg(SOA ? (c < 9 ? a.tri_a + (int64_t)c * a.n : a.tri_b + (int64_t)(c - 9) * a.n) + j
+                                         : (c < 9 ? a.tri_a + 9 * j + c : a.tri_b + 9 * j + (c - 9)));
+            const ServeOut so = ws_self_serve<T, STRICT, SOA, FULL, false>(&a, j, slot, scr_p);
+            tl.degenerate += so.flags & 1u;
+            if (so.flags & 2u) {
+                tl.comparison++;
+                tl.contacts += (so.flags >> 2) & 1u;
+                tl.intersecting += (so.flags >> 3) & 1u;
+                const double d = so.dist + 0.0;
+                tl.min_d = (d < tl.min_d) ? d : tl.min_d;
+            }
+        }
+        __syncwarp();
+    };
+    int cur = 0;
+    const int64_t wt0 = (int64_t)blockIdx.x * WQ_WARPS + wid;
+    issue_lane(wt0, wstash);
+    for (int64_t wt = wt0; wt < nwt; wt += wstep) {
+        const int64_t i = wt * 32 + lane;
+        T* const slot = wstash + cur * (18 * 32) + lane;
+        cp_async_wait_all();  // (a lane reads only the slots it copied itself)
+        cur ^= 1;
+        issue_lane(wt + wstep, wstash + cur * (18 * 32));
+        bool enq = false;
+        if (i < a.n) {
+            R A[9], B[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                A[k] = R(slot[k * 32]);
+                B[k] = R(slot[(9 + k) * 32]);
+            }
+            Rec<R> r;
+            run_iterative<32>(slot, A, B, [&] { return R(a.eps ? a.eps[i] : a.eps_scalar); }, kp, r);
+            tl.iterative++;
+            enq = r.kind == KIND_NOT_TERMINATED && (a.allow == nullptr || a.allow[i]);
+            // open pairs: a placeholder the warp overwrites when it serves its queue
+            if constexpr (FULL) store_rec_full<SOA, FULL>(a, i, r);
+            else store_rec<SOA>(a, i, r);
+            if (!enq) tl.result(r);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, enq);
+        if (m) {
+            if (enq) q[nq + __popc(m & ((1u << lane) - 1u))] = i;
+            nq += __popc(m);
+            __syncwarp();  // the queue entries and the placeholder rows before any lane serves them
+            if (nq >= 32) serve(32, slot);  // (the tile's slot is free now; nq < 32 before the push: nq <= 63)
+        }
+    }
+    cp_async_wait_all();
+    if (nq > 0) serve(nq, wstash + lane);
+    tl.flush<true, WQ_WARPS>(a.stats, a.hist, a.hist_host);
+}
+
 // ---- warp-specialised hybrid, warp-granular fallback (TC_WSW) ---------------------------
 // The same ring hand-over as hybrid_ws_kernel, but every fallback warp works
 // on its own: it claims 32 ring slots at a time, runs the degenerate screen
@@ -2163,8 +2277,8 @@ static int sm_count() {
 #endif
 struct FallbackHistory {
     enum Mode { PLAIN = 0, SELF = 1, FUSED = 2 };
-    unsigned long long* counters = nullptr;      // host-mapped copy {pairs, fallbacks, ring polls, self-served tiles}
-    unsigned long long* dev_counters = nullptr;  // the kernels' cumulative counters (device memory)
+    unsigned long long* counters = nullptr;      // host-mapped snapshot {seq, pairs, fallbacks, ring polls, self-served tiles, seq}
+    unsigned long long* dev_counters = nullptr;  // the kernels' cumulative counters + snapshot sequence (device memory)
     std::mutex mu;
     unsigned long long seen[4] = {0, 0, 0, 0};
     int cur = PLAIN;
@@ -2173,7 +2287,12 @@ struct FallbackHistory {
         if (!dev_counters) return PLAIN;
         std::lock_guard<std::mutex> lk(mu);
         unsigned long long c[4];
-        for (int k = 0; k < 4; ++k) c[k] = ((volatile unsigned long long*)counters)[k];
+        volatile unsigned long long* hh = counters;
+        const unsigned long long s_end = hh[5];
+        std::atomic_thread_fence(std::memory_order_acquire);
+        for (int k = 0; k < 4; ++k) c[k] = hh[1 + k];
+        std::atomic_thread_fence(std::memory_order_acquire);
+        if (hh[0] != s_end) return cur;  // a kernel is writing its snapshot: decide at the next launch
         if (c[0] >= seen[0] + 65536 && c[1] >= seen[1] && c[2] >= seen[2] && c[3] >= seen[3]) {
             const double pairs = (double)(c[0] - seen[0]), tiles = pairs / 32.0;
             const double rate = (double)(c[1] - seen[1]) / pairs;
@@ -2196,11 +2315,11 @@ static FallbackHistory& fallback_history() {
     FallbackHistory& h = hist[current_device()];
     std::call_once(h.once, [&h] {
         void *p = nullptr, *d = nullptr;
-        if (cudaHostAlloc(&p, 4 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) ==
+        if (cudaHostAlloc(&p, 6 * sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) ==
                 cudaSuccess &&
-            cudaMalloc(&d, 4 * sizeof(unsigned long long)) == cudaSuccess &&
-            cudaMemset(d, 0, 4 * sizeof(unsigned long long)) == cudaSuccess) {
-            memset(p, 0, 4 * sizeof(unsigned long long));
+            cudaMalloc(&d, 5 * sizeof(unsigned long long)) == cudaSuccess &&
+            cudaMemset(d, 0, 5 * sizeof(unsigned long long)) == cudaSuccess) {
+            memset(p, 0, 6 * sizeof(unsigned long long));
             h.counters = static_cast<unsigned long long*>(p);
             h.dev_counters = static_cast<unsigned long long*>(d);
         } else {
@@ -2286,6 +2405,9 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
                 aw.hist_host = fh.counters;
                 mode = TC_WS_SELF == 2 ? (int)FallbackHistory::SELF : fh.mode();
             }
+#ifdef TC_X_FORCE_MODE  // tests of one kernel on any batch (tools/libcmp.py)
+            mode = TC_X_FORCE_MODE;
+#endif
         }
         bool launched = false;
         if constexpr (WS) {
@@ -2310,8 +2432,23 @@ static int launch3(int variant, const Args<T>& a, cudaStream_t s) {
                 launched = true;
             }
         }
+        if constexpr (WS && TC_WQ) {
+            if (!launched) {
+                // few fallbacks: every warp iterates and serves its own queue of open pairs
+                const bool full = TC_WS_FULL && full_record(aw);
+                auto k = full ? hybrid_wq_kernel<T, STRICT, SOA, true> : hybrid_wq_kernel<T, STRICT, SOA, false>;
+                const size_t smem = wq_smem_bytes<T>();
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                const int64_t ctas = (aw.n + 32 * WQ_WARPS - 1) / (32 * WQ_WARPS);
+                int64_t g = ctas < sm_count() ? ctas : sm_count();
+                const int64_t cap = g_max_ctas.load(std::memory_order_relaxed);  // test knob
+                if (cap > 0 && g > cap) g = cap;
+                k<<<(unsigned)g, 32 * WQ_WARPS, smem, s>>>(aw);
+                launched = true;
+            }
+        }
         if (!launched) {
-            // the fused kernel: strict builds, and fast batches with few fallbacks
+            // the fused kernel: strict builds (and, without TC_WQ, fast batches with few fallbacks)
             auto k = hybrid_kernel<T, STRICT, SOA>;
 #ifndef TC_X_PAD
 #define TC_X_PAD 0
@@ -3117,7 +3254,7 @@ int tc_allreduce_stats(tc_stats* stats, void* nccl_comm, void* stream) {
 void tc_debug_set_max_ctas(int64_t max_ctas) { tc::g_max_ctas.store(max_ctas > 0 ? max_ctas : 0); }
 void tc_debug_fallback_history(uint64_t out[4]) {
     tc::FallbackHistory& h = tc::fallback_history();
-    for (int k = 0; k < 4; ++k) out[k] = h.counters ? ((volatile unsigned long long*)h.counters)[k] : 0;
+    for (int k = 0; k < 4; ++k) out[k] = h.counters ? ((volatile unsigned long long*)h.counters)[1 + k] : 0;
 }
 int tc_debug_fallback_rate_high(void) { return TC_WS_SELF == 1 && tc::fallback_history().high() ? 1 : 0; }
 int tc_debug_hybrid_mode(void) { return TC_WS_SELF == 1 ? tc::fallback_history().mode() : 0; }
