@@ -160,3 +160,73 @@ def test_blocks_degenerate_screen(oracle_lib, scene, strict):
                                               range(len(which)), T)
         assert [s["iterative"], s["comparison"], s["fallback"], s["degenerate"]] == list(counts[:4])
         assert np.array_equal(got["idx"], idx) and np.array_equal(got["distance"], dist)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json config 2 at its full size (16 x 16 x 8 particles of 320
+# triangles, 5,632 neighbour blocks, 576.7M triangle pairs) through
+# size-independent properties; tools/parity_cfg2.py compares every pair with
+# the oracle (profiles/r02_parity_cfg2.txt, two CPU-minutes) and stays a tool.
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def cfg2_full():
+    meshes, blocks, gaps = PT.cfg2_scene()
+    return meshes, blocks, gaps, torch.from_numpy(meshes).cuda()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("strict", [True, False])
+def test_cfg2_full_size_whole_equals_block_groups(cfg2_full, strict):
+    """One launch over all blocks == the launches over 8 contiguous groups of blocks:
+    summed counters, minimum distance and the (block, i, j)-ordered contact list, bit for bit."""
+    meshes, blocks, gaps, dmesh = cfg2_full
+    nb, T = blocks.shape[0], meshes.shape[1]
+    assert nb * T * T == 576_716_800
+    p = D.Params(n_iterative=16, epsilon=5e-2)
+    st = D.new_stats()
+    whole = PT.sort_contacts(PT.blocks_hybrid(dmesh, torch.from_numpy(blocks).cuda(), p, strict=strict, stats=st))
+    ws = D.read_stats(st)
+    assert ws["iterative"] == nb * T * T and ws["fallback"] == ws["comparison"] and ws["degenerate"] == 0
+    assert whole["n_contacts"] == ws["contacts"] > 10_000
+    assert ws["min_distance"] == float(whole["distance"].min())
+    assert np.all(whole["distance"] <= 2 * 5e-2)
+    parts, pstats = [], []
+    edges = np.linspace(0, nb, 9).astype(int)
+    for lo, hi in zip(edges[:-1], edges[1:]):
+        s = D.new_stats()
+        got = PT.sort_contacts(PT.blocks_hybrid(dmesh, torch.from_numpy(blocks[lo:hi]).cuda(), p, strict=strict,
+                                                stats=s))
+        got["idx"][:, 0] += lo
+        parts.append(got)
+        pstats.append(D.read_stats(s))
+    for k in ("iterative", "comparison", "fallback", "degenerate", "contacts", "intersecting"):
+        assert ws[k] == sum(s[k] for s in pstats), k
+    assert ws["min_distance"] == min(s["min_distance"] for s in pstats)
+    for k in ("idx", "distance", "point_a", "point_b"):
+        assert np.array_equal(whole[k], np.concatenate([q[k] for q in parts])), k
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_sampled_blocks_bitwise(oracle_lib, cfg2_full):
+    """Blocks sampled from the whole list (the ones with the most contacts among them): the
+    strict contacts of the full-scene launch, restricted to them, equal the oracle's."""
+    meshes, blocks, gaps, dmesh = cfg2_full
+    nb, T = blocks.shape[0], meshes.shape[1]
+    pkw = dict(n_iterative=16, epsilon=5e-2)
+    whole = PT.sort_contacts(PT.blocks_hybrid(dmesh, torch.from_numpy(blocks).cuda(), D.Params(**pkw), strict=True))
+    rng = np.random.default_rng(2)
+    # the three blocks with the most contacts, the first and last block, five random ones
+    blk, cnt = np.unique(whole["idx"][:, 0], return_counts=True)
+    busiest = blk[np.argsort(cnt)[-3:]]
+    which = sorted({*map(int, busiest), 0, nb - 1, *map(int, rng.integers(0, nb, 5))})
+    A, B = PT.block_pairs(meshes, blocks, which)
+    po = oracle_lib.make_params(**pkw)
+    ref, _, rc = oracle_lib.hybrid(A, B, po, po.epsilon, threads=oracle_lib.default_threads())
+    assert rc == 0
+    idx, dist, pa, pb = _contacts_from_flat(ref["kind"], ref["distance"], ref["point_a"], ref["point_b"], which, T)
+    sel = np.isin(whole["idx"][:, 0], which)
+    assert sel.sum() == len(idx) > 0
+    assert np.array_equal(whole["idx"][sel], idx)
+    assert np.array_equal(whole["distance"][sel], dist)
+    assert np.array_equal(whole["point_a"][sel], pa) and np.array_equal(whole["point_b"][sel], pb)
