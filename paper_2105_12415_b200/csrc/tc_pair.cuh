@@ -443,6 +443,14 @@ __device__ __forceinline__ void inside_point_params(const R* p, const Tri& tri, 
     const R kappa = R(T(sizeof(T) == 8 ? 1e-6 : 1e-2));
     if (!(det >= mulp(kappa, mulp(uu, vv))) || det == R(0)) {
         closest_point_params_t(p, tri, u, w);
+        // The region path's interior weights are ratios of cancelling products
+        // (va, vb, vc): on slivers in fp32 the FMA-contracted build returned
+        // weights tens of units outside the triangle (cfg3 slivers: the named
+        // point up to 44 L from the midpoint; the reference's own stay within
+        // 0.34 L).  A closest point lies on the triangle: clip to it (no change
+        // for weights already inside).
+        u = clipv(u, R(T(0)), R(T(1)));
+        w = clipv(w, R(T(0)), R(T(1)) - u);
         return;
     }
     const R r = rcpv(det);
