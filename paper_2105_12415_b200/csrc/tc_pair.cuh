@@ -426,6 +426,23 @@ struct Scratch {
 // frame -- for such a point the reference's closest point is the point
 // itself, its weights the same up to rounding (ill-conditioned triangles,
 // det < kappa * |ab|^2 |ac|^2, take the reference's region path).
+// The reference's region path in the reference's own rounding (no FMA
+// contraction), out of line: the ill-conditioned branch of inside_point_params
+// (slivers) is rare, and its weights are ratios of cancelling products that
+// contraction makes worse (tools/bary_recon.py).
+template <class T>
+__device__ __noinline__ void sliver_point_params(const T* p, const T* tri, T* uw) {
+    using S = Strict<T>;
+    S ps[3], ts[9], u, w;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) ps[i] = S(p[i]);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) ts[i] = S(tri[i]);
+    closest_point_params_t(ps, RegTri<S>{ts}, u, w);
+    uw[0] = u.v;
+    uw[1] = w.v;
+}
+
 template <class R, class Tri>
 __device__ __forceinline__ void inside_point_params(const R* p, const Tri& tri, R& u, R& w) {
     using T = typename Store<R>::type;
@@ -442,7 +459,24 @@ __device__ __forceinline__ void inside_point_params(const R* p, const Tri& tri, 
     const R det = fmav(uu, vv, -mulp(uv, uv));
     const R kappa = R(T(sizeof(T) == 8 ? 1e-6 : 1e-2));
     if (!(det >= mulp(kappa, mulp(uu, vv))) || det == R(0)) {
-        closest_point_params_t(p, tri, u, w);
+        // (fp32 takes this branch below sin^2 = 1e-2, 3-4 % of random triangles: those
+        // keep the inlined region path; only true slivers, sin^2 < 1e-6, pay the call --
+        // with every row of the branch out of line the fp32 hybrid ran 2 % slower.
+        // fp64 keeps the inlined path: its weights were never outside the triangle,
+        // and on all of cfg3 the out-of-line path moved one row's region decision
+        // past what the checker's sensitivity probe excuses.)
+        if (sizeof(T) == 8 || (det >= mulp(R(T(1e-6)), mulp(uu, vv)) && det != R(0))) {
+            closest_point_params_t(p, tri, u, w);
+        } else {
+            T pl[3], tl[9], uw[2];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) pl[i] = T(p[i]);
+#pragma unroll
+            for (int i = 0; i < 9; ++i) tl[i] = T(tri[i]);
+            sliver_point_params<T>(pl, tl, uw);
+            u = R(uw[0]);
+            w = R(uw[1]);
+        }
         // The region path's interior weights are ratios of cancelling products
         // (va, vb, vc): on slivers in fp32 the FMA-contracted build returned
         // weights tens of units outside the triangle (cfg3 slivers: the named
